@@ -1,0 +1,169 @@
+"""CPU oracle for the levelwise wavelet tree -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` and ``--impl reference`` legs) may import this package.
+The product package ``paper_1407_8142_b200`` never imports it, and the two
+share no code: the oracle is plain C (``wt_oracle.c``) that follows
+PAPER.md Fig. 1 (levelWT) step by step, plus this ctypes
+marshalling layer.
+
+``build(seq, sigma)`` returns a dict of numpy arrays laid out exactly as the
+C-ABI of the CUDA path specifies (``include/wt.h``), so the two can be
+compared element by element.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "wt_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+OK, EINVAL, ESYMBOL, ENOMEM = 0, -1, -2, -3
+
+
+class _Tree(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint64),
+        ("sigma", ctypes.c_uint64),
+        ("levels", ctypes.c_uint32),
+        ("elem_bytes", ctypes.c_uint32),
+        ("words_per_level", ctypes.c_uint64),
+        ("bits", ctypes.POINTER(ctypes.c_uint64)),
+        ("level_node_ptr", ctypes.POINTER(ctypes.c_uint64)),
+        ("node_key", ctypes.POINTER(ctypes.c_uint32)),
+        ("node_start", ctypes.POINTER(ctypes.c_uint32)),
+        ("total_nodes", ctypes.c_uint64),
+        ("blocks_per_level", ctypes.c_uint64),
+        ("supers_per_level", ctypes.c_uint64),
+        ("rank_block", ctypes.POINTER(ctypes.c_uint16)),
+        ("rank_super", ctypes.POINTER(ctypes.c_uint64)),
+    ]
+
+
+def compile_oracle(force: bool = False) -> str:
+    """Compile wt_oracle.c with gcc into oracle/liboracle.so (idempotent)."""
+    if (not force and os.path.exists(_LIB)
+            and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC)):
+        return _LIB
+    tmp = _LIB + f".tmp{os.getpid()}"
+    subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-Wextra", "-shared",
+                           "-fPIC", "-o", tmp, _SRC])
+    os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(compile_oracle())
+            lib.oracle_build.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
+                                         ctypes.c_uint64, ctypes.POINTER(ctypes.POINTER(_Tree))]
+            lib.oracle_build.restype = ctypes.c_int
+            lib.oracle_free.argtypes = [ctypes.POINTER(_Tree)]
+            lib.oracle_free.restype = None
+            lib.oracle_access.argtypes = [ctypes.POINTER(_Tree), ctypes.c_uint64]
+            lib.oracle_access.restype = ctypes.c_uint32
+            lib.oracle_rank.argtypes = [ctypes.POINTER(_Tree), ctypes.c_uint32, ctypes.c_uint64]
+            lib.oracle_rank.restype = ctypes.c_uint64
+            lib.oracle_rank1.argtypes = [ctypes.POINTER(_Tree), ctypes.c_uint32, ctypes.c_uint64]
+            lib.oracle_rank1.restype = ctypes.c_uint64
+            lib.oracle_levels.argtypes = [ctypes.c_uint64]
+            lib.oracle_levels.restype = ctypes.c_uint32
+            _lib = lib
+    return _lib
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int):
+        super().__init__(f"oracle_build failed with code {code}")
+        self.code = code
+
+
+def _copy(ptr, count, dtype):
+    if count == 0:
+        return np.zeros(0, dtype=dtype)
+    return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True)
+
+
+class OracleTree:
+    """Owns one C oracle tree; arrays are copied out into numpy."""
+
+    def __init__(self, seq: np.ndarray, sigma: int):
+        lib = _load()
+        seq = np.ascontiguousarray(seq)
+        if seq.dtype not in (np.uint8, np.uint16, np.uint32):
+            raise TypeError("seq must be uint8/uint16/uint32")
+        out = ctypes.POINTER(_Tree)()
+        rc = lib.oracle_build(seq.ctypes.data if seq.size else None, seq.size,
+                              seq.dtype.itemsize, int(sigma), ctypes.byref(out))
+        if rc != OK:
+            raise OracleError(rc)
+        self._lib = lib
+        self._t = out
+        t = out.contents
+        self.n, self.sigma, self.levels = t.n, t.sigma, t.levels
+        self.words_per_level = t.words_per_level
+        self.blocks_per_level = t.blocks_per_level
+        self.supers_per_level = t.supers_per_level
+        self.total_nodes = t.total_nodes
+
+    def arrays(self) -> dict:
+        t = self._t.contents
+        L = t.levels
+        return {
+            "bits": _copy(t.bits, L * t.words_per_level, np.uint64),
+            "level_node_ptr": _copy(t.level_node_ptr, L + 1, np.uint64),
+            "node_key": _copy(t.node_key, t.total_nodes, np.uint32),
+            "node_start": _copy(t.node_start, t.total_nodes, np.uint32),
+            "rank_block": _copy(t.rank_block, L * t.blocks_per_level, np.uint16),
+            "rank_super": _copy(t.rank_super, L * t.supers_per_level, np.uint64),
+        }
+
+    def access(self, positions) -> np.ndarray:
+        return np.array([self._lib.oracle_access(self._t, int(i)) for i in positions],
+                        dtype=np.uint32)
+
+    def rank(self, symbols, positions) -> np.ndarray:
+        return np.array([self._lib.oracle_rank(self._t, int(c), int(i))
+                         for c, i in zip(symbols, positions)], dtype=np.uint64)
+
+    def rank1(self, level: int, i: int) -> int:
+        return int(self._lib.oracle_rank1(self._t, level, i))
+
+    def close(self):
+        if getattr(self, "_t", None):
+            self._lib.oracle_free(self._t)
+            self._t = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def build(seq: np.ndarray, sigma: int) -> dict:
+    """Oracle construction; returns the §8(b) arrays plus scalar metadata."""
+    with OracleTree(seq, sigma) as t:
+        out = t.arrays()
+        out.update(n=t.n, sigma=t.sigma, levels=t.levels,
+                   words_per_level=t.words_per_level,
+                   blocks_per_level=t.blocks_per_level,
+                   supers_per_level=t.supers_per_level, total_nodes=t.total_nodes)
+    return out
+
+
+def levels(sigma: int) -> int:
+    return int(_load().oracle_levels(int(sigma)))

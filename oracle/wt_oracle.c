@@ -1,0 +1,317 @@
+/*
+ * wt_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU construction of the levelwise wavelet
+ * tree of arXiv 1407.8142 ("Parallel Wavelet Tree Construction").  It exists
+ * to prove the CUDA path right.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load it.  The product
+ * (paper_1407_8142_b200/) never links, imports or calls anything here, and
+ * this file shares no code, header, table or constant with it.
+ *
+ * What it computes (all citations are PAPER.md line numbers):
+ *   - L = ceil(log2 sigma); the root represents [0, 2^L - 1]          :217-218
+ *   - a node [a..b] has bit 0 for symbols in the lower half, 1 otherwise;
+ *     children are the two halves; stop when no symbols             :219-226
+ *   - levelWT, Fig. 1 (:330-380): per level, per node, mask
+ *     2^(L-(l+1)) (:333) selects the bit; X[i] = 1 for "left" symbols,
+ *     X = exclusive prefix sum, X_s its total (:347-352); a "right"
+ *     symbol goes to start + X_s + i - X[i], a "left" one to
+ *     start + X[i] (:353-360); children (start, X_s, 2id+1) and
+ *     (start + X_s, len - X_s, 2id+2) when non-empty (:363-371).
+ *     The recursion below visits nodes depth first, left before right,
+ *     so each level's node list comes out in ascending key order;
+ *     Fig. 1 builds the same lists breadth first (the filter of :375).
+ *   - node key p at level l: heap id 2^l - 1 + p (:418-420, :509, :536-539)
+ *   - rank directory: a prefix count of the level bitmap sampled at
+ *     two granularities (Jacobson, :805-814); reading R-9 fixes
+ *     the sampling: 512-bit blocks (u16, relative to the superblock) and
+ *     65536-bit superblocks (u64, absolute), plus the level total.
+ *   - access / rank_c by top-down descent (:204-211), using rank1 from the
+ *     directory above, so that brute-force query tests also pin the
+ *     directory.
+ *
+ * Parity status: every output array is pinned by tests/test_oracle_pins.py
+ * (closed forms, brute force, exhaustive tiny inputs); see DESIGN.md.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_OK 0
+#define OR_EINVAL (-1)
+#define OR_ESYMBOL (-2)
+#define OR_ENOMEM (-3)
+
+typedef struct {
+  uint64_t n;
+  uint64_t sigma;
+  uint32_t levels;
+  uint32_t elem_bytes;
+  uint64_t words_per_level;
+  uint64_t *bits;           /* levels * words_per_level, LSB-first       */
+  uint64_t *level_node_ptr; /* levels + 1, CSR offsets into node arrays  */
+  uint32_t *node_key;       /* top-l-bit prefix p of each non-empty node */
+  uint32_t *node_start;     /* first position of the node at its level   */
+  uint64_t total_nodes;
+  uint64_t blocks_per_level; /* ceil(n / 512)                            */
+  uint64_t supers_per_level; /* ceil(n / 65536) + 1                      */
+  uint16_t *rank_block;      /* levels * blocks_per_level                 */
+  uint64_t *rank_super;      /* levels * supers_per_level                 */
+} oracle_tree;
+
+/* growable (key, start) list for one level */
+typedef struct {
+  uint32_t *key;
+  uint32_t *start;
+  uint64_t len, cap;
+} node_list;
+
+typedef struct {
+  uint32_t L;
+  uint64_t wpl;
+  uint64_t *bits;
+  uint32_t *A;  /* the level's sequence S (Fig. 1 "S")   */
+  uint32_t *T;  /* the next level's sequence (Fig. 1 "S'") */
+  uint32_t *X;  /* prefix-sum array X of Fig. 1 l.12-14 (n < 2^32) */
+  node_list *nodes;
+  int oom;
+} builder;
+
+static int push_node(node_list *nl, uint32_t key, uint32_t start) {
+  if (nl->len == nl->cap) {
+    uint64_t nc = nl->cap ? nl->cap * 2 : 16;
+    uint32_t *k = (uint32_t *)realloc(nl->key, nc * sizeof(uint32_t));
+    if (!k) return -1;
+    nl->key = k;
+    uint32_t *s = (uint32_t *)realloc(nl->start, nc * sizeof(uint32_t));
+    if (!s) return -1;
+    nl->start = s;
+    nl->cap = nc;
+  }
+  nl->key[nl->len] = key;
+  nl->start[nl->len] = start;
+  nl->len++;
+  return 0;
+}
+
+/* visit(l, p, s, e): node with key p at level l covering positions [s, e). */
+static void visit(builder *b, uint32_t l, uint32_t p, uint64_t s, uint64_t e) {
+  if (b->oom) return;
+  if (s == e || l == b->L) return; /* no symbols, or below the last level */
+  if (push_node(&b->nodes[l], p, (uint32_t)s)) { b->oom = 1; return; }
+  uint32_t mask_shift = b->L - (l + 1);          /* mask = 2^(L-(l+1)), :333 */
+  uint64_t len = e - s;
+  uint64_t *B = b->bits + (uint64_t)l * b->wpl;  /* this level's bitmap     */
+  /* Fig. 1 l.12-13: X[i] = 1 if the symbol goes left (bit is 0) */
+  /* Fig. 1 l.14: exclusive prefix sum; X_s = total */
+  uint64_t Xs = 0;
+  for (uint64_t i = 0; i < len; i++) {
+    uint32_t left = ((b->A[s + i] >> mask_shift) & 1u) == 0;
+    b->X[s + i] = (uint32_t)Xs;
+    Xs += left;
+  }
+  /* Fig. 1 l.15-17: set the bit and move the symbol to S' */
+  for (uint64_t i = 0; i < len; i++) {
+    uint32_t sym = b->A[s + i];
+    if ((sym >> mask_shift) & 1u) {
+      uint64_t pos = s + i;
+      B[pos >> 6] |= (uint64_t)1 << (pos & 63);
+      b->T[s + Xs + i - b->X[s + i]] = sym;
+    } else {
+      b->T[s + b->X[s + i]] = sym;
+    }
+  }
+  memcpy(b->A + s, b->T + s, len * sizeof(uint32_t)); /* swap(S, S'), l.21 */
+  /* Fig. 1 l.18-19: children, ids 2id+1 / 2id+2 <=> keys 2p / 2p+1 */
+  if (Xs > 0) visit(b, l + 1, 2 * p, s, s + Xs);
+  if (len - Xs > 0) visit(b, l + 1, 2 * p + 1, s + Xs, e);
+}
+
+static uint32_t bitlen_minus1(uint64_t sigma) {
+  /* L = ceil(log2 sigma) = bit length of sigma - 1 (sigma >= 1) */
+  uint64_t v = sigma - 1;
+  uint32_t L = 0;
+  while (v) { L++; v >>= 1; }
+  return L;
+}
+
+static uint32_t popcount64(uint64_t w) { return (uint32_t)__builtin_popcountll(w); }
+
+void oracle_free(oracle_tree *t) {
+  if (!t) return;
+  free(t->bits);
+  free(t->level_node_ptr);
+  free(t->node_key);
+  free(t->node_start);
+  free(t->rank_block);
+  free(t->rank_super);
+  free(t);
+}
+
+uint32_t oracle_levels(uint64_t sigma) { return sigma ? bitlen_minus1(sigma) : 0; }
+
+int oracle_build(const void *seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma,
+                 oracle_tree **out) {
+  if (!out) return OR_EINVAL;
+  *out = NULL;
+  if ((n > 0 && !seq) || (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4))
+    return OR_EINVAL;
+  if (sigma < 1 || sigma > ((uint64_t)1 << (8 * elem_bytes)) || n >= ((uint64_t)1 << 32))
+    return OR_EINVAL;
+  uint32_t L = bitlen_minus1(sigma);
+
+  /* validation: every symbol must be < sigma (R-11) */
+  uint32_t *A = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+  if (!A) return OR_ENOMEM;
+  for (uint64_t i = 0; i < n; i++) {
+    uint32_t v;
+    if (elem_bytes == 1) v = ((const uint8_t *)seq)[i];
+    else if (elem_bytes == 2) v = ((const uint16_t *)seq)[i];
+    else v = ((const uint32_t *)seq)[i];
+    if ((uint64_t)v >= sigma) { free(A); return OR_ESYMBOL; }
+    A[i] = v;
+  }
+
+  oracle_tree *t = (oracle_tree *)calloc(1, sizeof(oracle_tree));
+  if (!t) { free(A); return OR_ENOMEM; }
+  t->n = n;
+  t->sigma = sigma;
+  t->levels = L;
+  t->elem_bytes = elem_bytes;
+  t->words_per_level = ((n + 511) / 512) * 8;
+  t->blocks_per_level = (n + 511) / 512;
+  t->supers_per_level = (n + 65535) / 65536 + 1;
+  uint64_t nbits = (uint64_t)L * t->words_per_level;
+  t->bits = (uint64_t *)calloc(nbits ? nbits : 1, sizeof(uint64_t));
+  t->level_node_ptr = (uint64_t *)calloc(L + 1, sizeof(uint64_t));
+  t->rank_block = (uint16_t *)calloc(L * t->blocks_per_level + 1, sizeof(uint16_t));
+  t->rank_super = (uint64_t *)calloc(L * t->supers_per_level + 1, sizeof(uint64_t));
+  builder b;
+  memset(&b, 0, sizeof(b));
+  b.L = L;
+  b.wpl = t->words_per_level;
+  b.bits = t->bits;
+  b.A = A;
+  b.T = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+  b.X = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+  b.nodes = (node_list *)calloc(L ? L : 1, sizeof(node_list));
+  if (!t->bits || !t->level_node_ptr || !t->rank_block || !t->rank_super || !b.T || !b.X ||
+      !b.nodes) {
+    free(A); free(b.T); free(b.X); free(b.nodes); oracle_free(t);
+    return OR_ENOMEM;
+  }
+
+  /* levelWT: A = {(0, n, 0, 2^L)} (Fig. 1 l.2) */
+  visit(&b, 0, 0, 0, n);
+  free(b.T);
+  free(b.X);
+  free(A);
+  if (b.oom) {
+    for (uint32_t l = 0; l < L; l++) { free(b.nodes[l].key); free(b.nodes[l].start); }
+    free(b.nodes);
+    oracle_free(t);
+    return OR_ENOMEM;
+  }
+
+  /* concatenate the per-level node lists (CSR) */
+  uint64_t total = 0;
+  for (uint32_t l = 0; l < L; l++) {
+    t->level_node_ptr[l] = total;
+    total += b.nodes[l].len;
+  }
+  t->level_node_ptr[L] = total;
+  t->total_nodes = total;
+  t->node_key = (uint32_t *)malloc((total ? total : 1) * sizeof(uint32_t));
+  t->node_start = (uint32_t *)malloc((total ? total : 1) * sizeof(uint32_t));
+  if (!t->node_key || !t->node_start) {
+    for (uint32_t l = 0; l < L; l++) { free(b.nodes[l].key); free(b.nodes[l].start); }
+    free(b.nodes);
+    oracle_free(t);
+    return OR_ENOMEM;
+  }
+  for (uint32_t l = 0; l < L; l++) {
+    uint64_t off = t->level_node_ptr[l];
+    if (b.nodes[l].len) {
+      memcpy(t->node_key + off, b.nodes[l].key, b.nodes[l].len * sizeof(uint32_t));
+      memcpy(t->node_start + off, b.nodes[l].start, b.nodes[l].len * sizeof(uint32_t));
+    }
+    free(b.nodes[l].key);
+    free(b.nodes[l].start);
+  }
+  free(b.nodes);
+
+  /* rank directory (:805-814 with reading R-9): walk the 512-bit blocks */
+  for (uint32_t l = 0; l < L; l++) {
+    const uint64_t *B = t->bits + (uint64_t)l * t->words_per_level;
+    uint16_t *blk = t->rank_block + (uint64_t)l * t->blocks_per_level;
+    uint64_t *sup = t->rank_super + (uint64_t)l * t->supers_per_level;
+    uint64_t ones = 0, base = 0;
+    for (uint64_t k = 0; k < t->blocks_per_level; k++) {
+      if (k % 128 == 0) { sup[k / 128] = ones; base = ones; }
+      blk[k] = (uint16_t)(ones - base);
+      for (int w = 0; w < 8; w++) ones += popcount64(B[k * 8 + w]);
+    }
+    sup[t->supers_per_level - 1] = ones; /* the level total */
+  }
+  *out = t;
+  return OR_OK;
+}
+
+/* rank1(l, i) = number of 1 bits of level l in positions [0, i) */
+static uint64_t rank1(const oracle_tree *t, uint32_t l, uint64_t i) {
+  if (i >= t->n) return t->rank_super[(uint64_t)l * t->supers_per_level + t->supers_per_level - 1];
+  const uint64_t *B = t->bits + (uint64_t)l * t->words_per_level;
+  uint64_t r = t->rank_super[(uint64_t)l * t->supers_per_level + (i >> 16)];
+  r += t->rank_block[(uint64_t)l * t->blocks_per_level + (i >> 9)];
+  uint64_t w0 = (i >> 9) * 8;
+  for (uint64_t w = w0; w < (i >> 6); w++) r += popcount64(B[w]);
+  if (i & 63) r += popcount64(B[i >> 6] & (((uint64_t)1 << (i & 63)) - 1));
+  return r;
+}
+
+uint64_t oracle_rank1(const oracle_tree *t, uint32_t level, uint64_t i) {
+  if (!t || level >= t->levels || i > t->n) return UINT64_MAX;
+  return rank1(t, level, i);
+}
+
+/* access(S, i) (:204-205): descend, remapping i into the child's range */
+uint32_t oracle_access(const oracle_tree *t, uint64_t i) {
+  if (!t || i >= t->n) return UINT32_MAX;
+  uint64_t s = 0, e = t->n;
+  uint32_t sym = 0;
+  for (uint32_t l = 0; l < t->levels; l++) {
+    uint64_t r1s = rank1(t, l, s), r1e = rank1(t, l, e), r1i = rank1(t, l, i);
+    uint64_t z = (e - s) - (r1e - r1s); /* zeros in the node = left child size */
+    const uint64_t *B = t->bits + (uint64_t)l * t->words_per_level;
+    uint32_t bit = (uint32_t)((B[i >> 6] >> (i & 63)) & 1u);
+    sym = (sym << 1) | bit;
+    if (bit) {
+      i = s + z + (r1i - r1s);
+      s = s + z;
+    } else {
+      i = s + ((i - s) - (r1i - r1s));
+      e = s + z;
+    }
+  }
+  return sym;
+}
+
+/* rank_c(S, i) (:205-206): occurrences of c in positions 0..i inclusive */
+uint64_t oracle_rank(const oracle_tree *t, uint32_t c, uint64_t i) {
+  if (!t || i >= t->n || (uint64_t)c >= t->sigma) return UINT64_MAX;
+  uint64_t s = 0, e = t->n, r = i + 1; /* r = count of the prefix [s, s+r) */
+  for (uint32_t l = 0; l < t->levels; l++) {
+    uint64_t r1s = rank1(t, l, s), r1e = rank1(t, l, e), r1p = rank1(t, l, s + r);
+    uint64_t z = (e - s) - (r1e - r1s);
+    uint32_t bit = (c >> (t->levels - 1 - l)) & 1u;
+    if (bit) {
+      r = r1p - r1s;
+      s = s + z;
+    } else {
+      r = r - (r1p - r1s);
+      e = s + z;
+    }
+    if (r == 0) return 0;
+  }
+  return r;
+}
