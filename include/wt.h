@@ -1,0 +1,159 @@
+/*
+ * wt.h -- C ABI of the B200 (sm_100a) levelwise wavelet-tree builder.
+ *
+ * The operation is the construction of arXiv 1407.8142 ("Parallel Wavelet
+ * Tree Construction"), levelWT (Fig. 1): for an
+ * integer sequence S of length n over the alphabet [0, sigma) (PAPER.md:
+ * 201-203), L = ceil(log2 sigma) levels; level l
+ * stores, for every element of S_l = S stably sorted by its top l bits
+ * (PAPER.md:468-475), the element's (l+1)'st highest bit (mask
+ * 2^(L-(l+1))); each node's sub-sequence is stably
+ * split by that bit; the level's non-empty nodes
+ * and a two-level rank directory are
+ * emitted.  Queries follow PAPER.md:204-208.
+ *
+ * All pointers in this header are plain pointers; no C++ or torch types.
+ * "Device pointer" means CUDA global memory of the current device.  Streams
+ * are passed as `void*` holding a cudaStream_t (NULL = legacy default stream).
+ *
+ * Normative output layout ("Output layout"):
+ *   bits      u64[levels * words_per_level], words_per_level = ceil(n/512)*8.
+ *             Bit i of level l = (bits[l*WPL + (i>>6)] >> (i & 63)) & 1
+ *             (LSB first, reading R-1).  Padding bits are 0.
+ *   nodes     CSR over levels: level_node_ptr u64[levels+1]; entries
+ *             j in [ptr[l], ptr[l+1]) are the level's non-empty nodes in
+ *             ascending key order: node_key[j] = p (the node's top-l-bit
+ *             prefix; heap id 2^l - 1 + p),
+ *             node_start[j] = position of its first element at level l.
+ *             A node's length is the next start (or n) minus its start.
+ *   rank      blocks_per_level = ceil(n/512), supers_per_level =
+ *             ceil(n/65536) + 1.  rank_super[l*SPL + s] = number of 1 bits
+ *             of level l in [0, min(s*65536, n)) (last entry = level total);
+ *             rank_block[l*BPL + b] = number of 1 bits in
+ *             [floor(b/128)*65536, b*512) (always < 65536).
+ *             rank1(l, i) = super[i>>16] + block[i>>9]
+ *                         + popc(words of the block before word i>>6)
+ *                         + popc(bits[i>>6] & ((1<<(i&63)) - 1)).
+ */
+#ifndef WT_B200_H
+#define WT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes. */
+#define WT_OK 0
+#define WT_EINVAL (-1)      /* null pointer, bad elem_bytes/sigma, n out of range   */
+#define WT_ESYMBOL (-2)     /* some S[i] >= sigma; no tree is produced              */
+#define WT_ENOMEM (-3)      /* device (or pinned host) allocation failed            */
+#define WT_ECUDA (-4)       /* a CUDA runtime call or kernel launch failed          */
+#define WT_EUNSUPPORTED (-5)/* valid input this build cannot handle yet (see below) */
+
+/* Read-only view of a built tree.  Every array pointer is a DEVICE pointer
+ * owned by the library; it stays valid until wt_free(). */
+typedef struct wt_tree {
+  uint64_t n;                 /* sequence length                              */
+  uint64_t sigma;             /* alphabet size                                */
+  uint32_t levels;            /* L = ceil(log2 sigma) (0 when sigma == 1)     */
+  uint32_t elem_bytes;        /* bytes per input symbol: 1, 2 or 4            */
+  uint64_t words_per_level;   /* ceil(n/512) * 8                              */
+  uint64_t *bits;             /* u64[levels * words_per_level]                */
+  uint64_t *level_node_ptr;   /* u64[levels + 1]                              */
+  uint32_t *node_key;         /* u32[total_nodes]                             */
+  uint32_t *node_start;       /* u32[total_nodes]                             */
+  uint64_t total_nodes;       /* level_node_ptr[levels]                       */
+  uint64_t blocks_per_level;  /* ceil(n/512)                                  */
+  uint64_t supers_per_level;  /* ceil(n/65536) + 1                            */
+  uint16_t *rank_block;       /* u16[levels * blocks_per_level]               */
+  uint64_t *rank_super;       /* u64[levels * supers_per_level]               */
+  void *internal;             /* library bookkeeping; do not touch            */
+} wt_tree;
+
+/*
+ * wt_build -- build the wavelet tree of S (Fig. 1; SURVEY §8(a)
+ * steps A1-A7).
+ *   d_seq      DEVICE pointer to n symbols of elem_bytes bytes each
+ *              (little-endian unsigned).  Caller-owned, read-only, not
+ *              retained after return.  Any alignment is accepted.
+ *   n          sequence length; 0 <= n < 2^30 in this build (larger n
+ *              returns WT_EUNSUPPORTED).
+ *   elem_bytes 1, 2 or 4.
+ *   sigma      alphabet size, 1 <= sigma <= 2^(8*elem_bytes); this build
+ *              supports L = ceil(log2 sigma) <= 16 (larger: WT_EUNSUPPORTED).
+ *   stream     cudaStream_t (as void*) on which all work is enqueued.
+ *   out        receives the tree on success, NULL on any error.
+ * Work is enqueued on `stream`, which is then synchronised ONCE to read the
+ * error flag and the per-level node counts; on WT_OK the tree is complete
+ * and immutable.  Output memory is stream-ordered device memory owned by the
+ * library and released only by wt_free().  On error nothing leaks.
+ * n == 0 gives empty levels; sigma == 1 gives a tree with 0 levels.
+ */
+int wt_build(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma,
+             void *stream, wt_tree **out);
+
+/*
+ * wt_build_host -- as wt_build, but h_seq is a HOST pointer (pinned memory
+ * gives full PCIe bandwidth; pageable memory is accepted).  The host->device
+ * copy is enqueued on `stream` inside the call; everything else is identical
+ * (the end-to-end path measured by bench.py's "e2e").
+ */
+int wt_build_host(const void *h_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma,
+                  void *stream, wt_tree **out);
+
+/* wt_free -- release everything owned by t (synchronises the device as
+ * needed).  NULL is a no-op.  Returns WT_OK or WT_ECUDA. */
+int wt_free(wt_tree *t);
+
+/*
+ * wt_access -- batched access(S, i) (batched queries
+ * PAPER.md:275-277).  d_pos: DEVICE u64[q] positions; d_out: DEVICE u32[q]
+ * receives S[pos[k]], or UINT32_MAX when pos[k] >= n.  Asynchronous on
+ * `stream`; caller owns both buffers.  WT_EINVAL on null t, or null buffers
+ * with q > 0.
+ */
+int wt_access(const wt_tree *t, const uint64_t *d_pos, uint64_t q, uint32_t *d_out,
+              void *stream);
+
+/*
+ * wt_rank -- batched rank_c(S, i) = #{ j <= i : S[j] == c } (inclusive,
+ * PAPER.md:205-206).  d_sym: DEVICE u32[q] symbols c; d_pos: DEVICE u64[q];
+ * d_out: DEVICE u64[q], UINT64_MAX when pos >= n or c >= sigma.
+ * Asynchronous; errors as wt_access.
+ */
+int wt_rank(const wt_tree *t, const uint32_t *d_sym, const uint64_t *d_pos, uint64_t q,
+            uint64_t *d_out, void *stream);
+
+/* ---- measurement hooks (used by bench.py; no effect on results) ---- */
+
+#define WT_PROF_MAX 32
+typedef struct wt_prof_entry {
+  char name[40];          /* kernel name                                    */
+  float ms;               /* summed device time of its launches (CUDA events
+                             recorded on the launch stream)                 */
+  uint32_t launches;      /* launches in the last profiled build            */
+  uint32_t pad;
+  uint64_t algo_bytes;    /* algorithmic bytes moved by those launches
+                                             */
+} wt_prof_entry;
+
+typedef struct wt_profile {
+  uint32_t count;               /* valid entries                            */
+  uint32_t total_launches;      /* all kernel launches of the last build    */
+  wt_prof_entry e[WT_PROF_MAX];
+} wt_profile;
+
+/* Enable (1) / disable (0) per-kernel event timing in subsequent builds. */
+int wt_profile_enable(int on);
+/* Copy the per-kernel record of the most recent build (profiled or not:
+ * launches and total_launches are always filled, ms only when enabled). */
+int wt_last_profile(wt_profile *out);
+/* Version string of the library. */
+const char *wt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WT_B200_H */

@@ -1,0 +1,268 @@
+"""ctypes binding of include/wt.h (argument marshalling only).
+
+Every step of the build runs in ``libwt_b200.so``; torch is used for device
+memory, streams and zero-copy tensor views of the library-owned outputs.
+Names follow the C ABI: ``build`` -> ``wt_build``, ``build_host`` ->
+``wt_build_host``, ``access`` -> ``wt_access``, ``rank`` -> ``wt_rank``,
+``free`` -> ``wt_free``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libwt_b200.so")
+
+WT_OK, WT_EINVAL, WT_ESYMBOL, WT_ENOMEM, WT_ECUDA, WT_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
+_NAMES = {WT_EINVAL: "WT_EINVAL", WT_ESYMBOL: "WT_ESYMBOL", WT_ENOMEM: "WT_ENOMEM",
+          WT_ECUDA: "WT_ECUDA", WT_EUNSUPPORTED: "WT_EUNSUPPORTED"}
+
+
+class WtError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what} failed: {_NAMES.get(code, code)}")
+        self.code = code
+
+
+class _WtTree(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint64), ("sigma", ctypes.c_uint64),
+        ("levels", ctypes.c_uint32), ("elem_bytes", ctypes.c_uint32),
+        ("words_per_level", ctypes.c_uint64),
+        ("bits", ctypes.c_void_p), ("level_node_ptr", ctypes.c_void_p),
+        ("node_key", ctypes.c_void_p), ("node_start", ctypes.c_void_p),
+        ("total_nodes", ctypes.c_uint64),
+        ("blocks_per_level", ctypes.c_uint64), ("supers_per_level", ctypes.c_uint64),
+        ("rank_block", ctypes.c_void_p), ("rank_super", ctypes.c_void_p),
+        ("internal", ctypes.c_void_p),
+    ]
+
+
+class _ProfEntry(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 40), ("ms", ctypes.c_float), ("launches", ctypes.c_uint32),
+                ("pad", ctypes.c_uint32), ("algo_bytes", ctypes.c_uint64)]
+
+
+class _Profile(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_uint32), ("total_launches", ctypes.c_uint32),
+                ("e", _ProfEntry * 32)]
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run `python __graft_entry__.py build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P = ctypes.POINTER(_WtTree)
+    lib.wt_build.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                             ctypes.c_void_p, ctypes.POINTER(P)]
+    lib.wt_build.restype = ctypes.c_int
+    lib.wt_build_host.argtypes = lib.wt_build.argtypes
+    lib.wt_build_host.restype = ctypes.c_int
+    lib.wt_free.argtypes = [P]
+    lib.wt_free.restype = ctypes.c_int
+    lib.wt_access.argtypes = [P, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+    lib.wt_access.restype = ctypes.c_int
+    lib.wt_rank.argtypes = [P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                            ctypes.c_void_p]
+    lib.wt_rank.restype = ctypes.c_int
+    lib.wt_profile_enable.argtypes = [ctypes.c_int]
+    lib.wt_profile_enable.restype = ctypes.c_int
+    lib.wt_last_profile.argtypes = [ctypes.POINTER(_Profile)]
+    lib.wt_last_profile.restype = ctypes.c_int
+    lib.wt_version.argtypes = []
+    lib.wt_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+class _CAI:
+    """Minimal __cuda_array_interface__ wrapper for a library-owned array."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
+                                         "data": (int(ptr or 0), False), "version": 3,
+                                         "strides": None}
+
+
+def _view(ptr, count, typestr, dtype, device):
+    if count == 0 or not ptr:
+        return torch.zeros(0, dtype=dtype, device=device)
+    return torch.as_tensor(_CAI(ptr, count, typestr), device=device)
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class WaveletTree:
+    """A built tree.  Arrays are zero-copy torch views of library memory and
+    stay valid until ``free()`` (called on garbage collection too)."""
+
+    def __init__(self, handle, device):
+        self._h = handle
+        t = handle.contents
+        self.device = device
+        self.n, self.sigma, self.levels = int(t.n), int(t.sigma), int(t.levels)
+        self.elem_bytes = int(t.elem_bytes)
+        self.words_per_level = int(t.words_per_level)
+        self.blocks_per_level = int(t.blocks_per_level)
+        self.supers_per_level = int(t.supers_per_level)
+        self.total_nodes = int(t.total_nodes)
+        L = self.levels
+        self.bits = _view(t.bits, L * self.words_per_level, "<u8", torch.uint64, device)
+        self.level_node_ptr = _view(t.level_node_ptr, L + 1, "<u8", torch.uint64, device)
+        self.node_key = _view(t.node_key, self.total_nodes, "<u4", torch.uint32, device)
+        self.node_start = _view(t.node_start, self.total_nodes, "<u4", torch.uint32, device)
+        self.rank_block = _view(t.rank_block, L * self.blocks_per_level, "<u2", torch.uint16, device)
+        self.rank_super = _view(t.rank_super, L * self.supers_per_level, "<u8", torch.uint64, device)
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("tree already freed")
+        return self._h
+
+    def numpy(self) -> dict:
+        """Copy every output array to host numpy (for bit-exact comparison)."""
+        out = {}
+        for k in ("bits", "level_node_ptr", "node_key", "node_start", "rank_block", "rank_super"):
+            out[k] = getattr(self, k).cpu().numpy()
+        out.update(n=self.n, sigma=self.sigma, levels=self.levels,
+                   words_per_level=self.words_per_level, blocks_per_level=self.blocks_per_level,
+                   supers_per_level=self.supers_per_level, total_nodes=self.total_nodes)
+        return out
+
+    def access(self, pos: torch.Tensor, stream=None) -> torch.Tensor:
+        return access(self, pos, stream)
+
+    def rank(self, sym: torch.Tensor, pos: torch.Tensor, stream=None) -> torch.Tensor:
+        return rank(self, sym, pos, stream)
+
+    def free(self):
+        if self._h is not None:
+            for k in ("bits", "level_node_ptr", "node_key", "node_start", "rank_block", "rank_super"):
+                setattr(self, k, None)
+            rc = _load().wt_free(self._h)
+            self._h = None
+            if rc != WT_OK:
+                raise WtError(rc, "wt_free")
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _elem_bytes(t: torch.Tensor) -> int:
+    eb = t.element_size()
+    if eb not in (1, 2, 4) or t.dtype.is_floating_point:
+        raise TypeError("sequence must be an 8/16/32-bit integer tensor")
+    return eb
+
+
+def build(seq: torch.Tensor, sigma: int, stream=None) -> WaveletTree:
+    """wt_build on a CUDA tensor holding S (any 8/16/32-bit integer dtype,
+    read as unsigned)."""
+    lib = _load()
+    if not seq.is_cuda:
+        raise ValueError("build() needs a CUDA tensor; use build_host() for host data")
+    seq = seq.contiguous().view(-1)
+    out = ctypes.POINTER(_WtTree)()
+    rc = lib.wt_build(ctypes.c_void_p(seq.data_ptr() if seq.numel() else 0), seq.numel(),
+                      _elem_bytes(seq), int(sigma), ctypes.c_void_p(_stream_ptr(stream)),
+                      ctypes.byref(out))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_build")
+    return WaveletTree(out, seq.device)
+
+
+def build_host(seq, sigma: int, stream=None, device=None) -> WaveletTree:
+    """wt_build_host: seq is a host numpy array or CPU tensor (pinned is fastest)."""
+    lib = _load()
+    if isinstance(seq, torch.Tensor):
+        if seq.is_cuda:
+            raise ValueError("build_host() needs host memory")
+        seq = seq.contiguous().view(-1)
+        ptr, cnt, eb = seq.data_ptr(), seq.numel(), _elem_bytes(seq)
+    else:
+        import numpy as np
+        seq = np.ascontiguousarray(seq)
+        if seq.dtype not in (np.uint8, np.uint16, np.uint32, np.int8, np.int16, np.int32):
+            raise TypeError("sequence must be an 8/16/32-bit integer array")
+        ptr, cnt, eb = seq.ctypes.data, seq.size, seq.dtype.itemsize
+    out = ctypes.POINTER(_WtTree)()
+    rc = lib.wt_build_host(ctypes.c_void_p(ptr if cnt else 0), cnt, eb, int(sigma),
+                           ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_build_host")
+    return WaveletTree(out, device or torch.device("cuda", torch.cuda.current_device()))
+
+
+def access(tree: WaveletTree, pos: torch.Tensor, stream=None) -> torch.Tensor:
+    """wt_access: pos int64/uint64 CUDA tensor -> uint32 symbols (int64 view returned)."""
+    lib = _load()
+    pos = pos.contiguous().view(-1)
+    out = torch.empty(pos.numel(), dtype=torch.int32, device=pos.device)
+    rc = lib.wt_access(tree.handle, ctypes.c_void_p(pos.data_ptr() if pos.numel() else 0), pos.numel(),
+                       ctypes.c_void_p(out.data_ptr() if out.numel() else 0),
+                       ctypes.c_void_p(_stream_ptr(stream)))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_access")
+    return out.view(torch.uint32)
+
+
+def rank(tree: WaveletTree, sym: torch.Tensor, pos: torch.Tensor, stream=None) -> torch.Tensor:
+    """wt_rank: inclusive rank_c(S, i); sym int32/uint32, pos int64/uint64 CUDA tensors."""
+    lib = _load()
+    sym = sym.contiguous().view(-1)
+    pos = pos.contiguous().view(-1)
+    if sym.numel() != pos.numel():
+        raise ValueError("sym and pos must have the same length")
+    out = torch.empty(pos.numel(), dtype=torch.int64, device=pos.device)
+    rc = lib.wt_rank(tree.handle, ctypes.c_void_p(sym.data_ptr() if sym.numel() else 0),
+                     ctypes.c_void_p(pos.data_ptr() if pos.numel() else 0), pos.numel(),
+                     ctypes.c_void_p(out.data_ptr() if out.numel() else 0),
+                     ctypes.c_void_p(_stream_ptr(stream)))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_rank")
+    return out.view(torch.uint64)
+
+
+def free(tree: WaveletTree) -> None:
+    tree.free()
+
+
+def profile_enable(on: bool = True) -> None:
+    _load().wt_profile_enable(1 if on else 0)
+
+
+def last_profile() -> dict:
+    p = _Profile()
+    _load().wt_last_profile(ctypes.byref(p))
+    ents = []
+    for i in range(p.count):
+        e = p.e[i]
+        ents.append({"name": e.name.decode(), "ms": float(e.ms), "launches": int(e.launches),
+                     "algo_bytes": int(e.algo_bytes)})
+    return {"total_launches": int(p.total_launches), "kernels": ents}
+
+
+def version() -> str:
+    return _load().wt_version().decode()
