@@ -5,9 +5,13 @@
 // The stream is synchronised exactly once, at the end, to read the error flag
 // and the node counts.
 #include "wt.h"
-#include "wt_device.cuh"
+#include "wt_group.cuh"
+#include "wt_prep.cuh"
+#include "wt_rank.cuh"
 
 #include <cstdio>
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -147,23 +151,44 @@ struct Allocs {
   }
 };
 
-template <typename InT, typename RecT, bool HAS_OUT>
-cudaError_t launch_group(const GroupParams &gp, cudaStream_t s, int grid) {
-  const size_t smem = 4 * sizeof(WarpSmem<RecT>);
-  auto kern = k_group<InT, RecT, HAS_OUT>;
+template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
+cudaError_t launch_group(const GroupParams &gp, cudaStream_t s) {
+  const size_t smem = GROUP_WARPS * sizeof(WarpSmem<RecT>);
+  auto kern = k_group<InT, RecT, OutT, HAS_OUT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, 128, smem, s>>>(gp);
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GROUP_WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  kern<<<num_sms() * per_sm, GROUP_WARPS * 32, smem, s>>>(gp);
   return cudaGetLastError();
 }
 
-template <typename RecT>
-int group_grid() {
-  const size_t smem = 4 * sizeof(WarpSmem<RecT>);
-  int per_sm = (int)((227 * 1024) / (smem + 1024));
-  if (per_sm < 1) per_sm = 1;
-  return num_sms() * per_sm;
-}
+// Per-group scratch: chains, claim order, digit tables.
+struct GroupBufs {
+  uint32_t tau = 0, l0 = 0, pbits = 0, ndig = 0;
+  uint64_t max_chains = 0, max_tiles = 0, max_rows = 0;
+  uint32_t *chain_begin = nullptr, *chain_end = nullptr, *chain_key = nullptr, *chain_row = nullptr;
+  uint32_t *row_start = nullptr, *chain_prefix = nullptr, *tile_base = nullptr;
+  uint32_t *hnt = nullptr, *tie = nullptr, *cum = nullptr, *Cseg = nullptr;
+  uint32_t *scalars = nullptr;  // [0] nchains, [1] total tiles, [2] tile counter, [3] nrows
+  uint2 *claim = nullptr;
+  void alloc(Allocs &A) {
+    chain_begin = A.alloc<uint32_t>(max_chains, false);
+    chain_end = A.alloc<uint32_t>(max_chains, false);
+    chain_key = A.alloc<uint32_t>(max_chains, false);
+    chain_row = A.alloc<uint32_t>(max_chains, false);
+    row_start = A.alloc<uint32_t>(max_rows, false);
+    tile_base = A.alloc<uint32_t>(max_chains, false);
+    hnt = A.alloc<uint32_t>(max_tiles + 2, false);
+    tie = A.alloc<uint32_t>(max_tiles + 2, false);
+    cum = A.alloc<uint32_t>(max_tiles + 2, false);
+    Cseg = A.alloc<uint32_t>(max_rows * (ndig + 1), false);
+    scalars = A.alloc<uint32_t>(4, false);
+    claim = A.alloc<uint2>(max_tiles, false);
+  }
+};
 
 int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n, uint32_t eb,
                uint64_t sigma, void *stream_v, wt_tree **out) {
@@ -209,7 +234,6 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   t->rank_block = A.alloc<uint16_t>(L * BPL, true);
   t->rank_super = A.alloc<uint64_t>(L * SPL, true);
 
-  // scratch
   const void *seq = d_seq;
   if (from_host) {
     void *d = A.alloc<uint8_t>(n * eb, false);
@@ -218,29 +242,41 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     }
     seq = d;
   }
-  const uint32_t Lh = L;  // L <= 16: the histogram covers every level
-  const uint32_t nbins = 1u << Lh;
-  const bool pair16 = Lh > 15;
-  const int hist_ctas = num_sms() * (pair16 ? 1 : 2);
+
+  // ---- plan: groups of <= 8 levels; A1 chunks are the group-0 chains ----
+  const uint32_t NG = (L + TAU_MAX - 1) / TAU_MAX;
+  GroupBufs G[2];
+  const uint64_t ntiles_n = std::max<uint64_t>((n + TW - 1) / TW, 1);
+  uint32_t K = (uint32_t)std::min<uint64_t>((uint64_t)num_sms() * 2, ntiles_n);
+  const uint64_t CH = ((ntiles_n + K - 1) / K) * TW;
+  K = (uint32_t)std::max<uint64_t>((n + CH - 1) / CH, 1);
+  for (uint32_t g = 0; g < NG; g++) {
+    GroupBufs &gb = G[g];
+    gb.l0 = g * TAU_MAX;
+    gb.tau = std::min<uint32_t>(TAU_MAX, L - gb.l0);
+    gb.pbits = L - gb.l0 - gb.tau;
+    gb.ndig = 1u << gb.tau;
+    if (g == 0) {
+      gb.max_chains = K;
+      gb.max_rows = 1;
+      gb.max_tiles = ntiles_n + 1;
+    } else {
+      gb.max_chains = std::min<uint64_t>(1ull << gb.l0, std::max<uint64_t>(n, 1));
+      gb.max_rows = gb.max_chains;
+      gb.max_tiles = ntiles_n + gb.max_chains + 1;
+    }
+    gb.alloc(A);
+  }
   uint32_t *err = A.alloc<uint32_t>(4, false);
-  uint32_t *partial = A.alloc<uint32_t>((uint64_t)hist_ctas * nbins, false);
-  uint32_t *adj = A.alloc<uint32_t>(nbins, false);
-  uint32_t *hist = A.alloc<uint32_t>(nbins, false);
-  uint32_t *Hx = A.alloc<uint32_t>(nbins + 1, false);
+  uint32_t *partial = A.alloc<uint32_t>((uint64_t)K * NDIG, false);
+  if (NG) G[0].chain_prefix = A.alloc<uint32_t>((uint64_t)K * NDIG, false);
   uint32_t *ncount = A.alloc<uint32_t>(L + 1, false);
   uint32_t *blkcnt = A.alloc<uint32_t>(L * BPL, false);
   uint64_t *suptot = A.alloc<uint64_t>(L * NSD, false);
-  const uint32_t tau0 = L < 8 ? L : 8;
-  const uint32_t tau1 = L - tau0;
-  const uint64_t max_tiles0 = (n + TW - 1) / TW;
-  const uint64_t max_tiles1 = tau1 ? (n + TW - 1) / TW + std::min<uint64_t>(1ull << tau0, n) : 0;
-  const uint64_t max_tiles = std::max(max_tiles0, max_tiles1);
+  uint64_t max_tiles = 1;
+  for (uint32_t g = 0; g < NG; g++) max_tiles = std::max(max_tiles, G[g].max_tiles);
   uint32_t *state = A.alloc<uint32_t>(max_tiles * NDIG, false);
-  uint32_t *counters = A.alloc<uint32_t>(4, false);
-  uint8_t *keys1 = tau1 ? A.alloc<uint8_t>(n, false) : nullptr;
-  uint32_t *tile_seg = tau1 ? A.alloc<uint32_t>(max_tiles1, false) : nullptr;
-  uint32_t *seg_tile_base = tau1 ? A.alloc<uint32_t>(std::min<uint64_t>(1ull << tau0, n) + 1, false) : nullptr;
-  uint32_t *total_tiles = counters + 2;
+  void *keys1 = NG > 1 ? (void *)A.alloc<uint8_t>(n, false) : nullptr;
 
   static uint64_t *h_stage = nullptr;  // pinned staging for the single D2H
   static std::mutex stage_mu;
@@ -248,123 +284,148 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     std::lock_guard<std::mutex> g(stage_mu);
     if (!h_stage && cudaMallocHost(&h_stage, 64 * sizeof(uint64_t)) != cudaSuccess) A.fail = true;
   }
-
-  auto fail_out = [&](int code) {
+  if (A.fail) {
     A.free_scratch();
     A.free_outputs();
     cudaStreamSynchronize(s);
     rec.discard();
     delete t;
-    return code;
-  };
-  if (A.fail) return fail_out(WT_ENOMEM);
-
-  cudaError_t ce = cudaSuccess;
-  auto chk = [&](cudaError_t e) { if (e != cudaSuccess && ce == cudaSuccess) ce = e; };
-
-  chk(cudaMemsetAsync(err, 0, 4 * sizeof(uint32_t), s));
-  chk(cudaMemsetAsync(counters, 0, 4 * sizeof(uint32_t), s));
-  chk(cudaMemsetAsync(adj, 0, nbins * sizeof(uint32_t), s));
-  chk(cudaMemsetAsync(t->level_node_ptr, 0, (L + 1) * sizeof(uint64_t), s));
-  if (L) {
-    chk(cudaMemsetAsync(t->bits, 0, L * WPL * sizeof(uint64_t), s));
-    chk(cudaMemsetAsync(blkcnt, 0, L * BPL * sizeof(uint32_t), s));
-    if (max_tiles) chk(cudaMemsetAsync(state, 0, max_tiles * NDIG * sizeof(uint32_t), s));
+    return WT_ENOMEM;
   }
 
-  // ---- A1: validate + histogram ----
+  cudaError_t ce = cudaSuccess;
+  auto chk = [&](cudaError_t e) {
+    if (e != cudaSuccess && ce == cudaSuccess) ce = e;
+  };
+
+  chk(cudaMemsetAsync(err, 0, 4 * sizeof(uint32_t), s));
+  chk(cudaMemsetAsync(t->level_node_ptr, 0, (L + 1) * sizeof(uint64_t), s));
+  if (L && n) {
+    chk(cudaMemsetAsync(t->bits, 0, L * WPL * sizeof(uint64_t), s));
+    chk(cudaMemsetAsync(blkcnt, 0, L * BPL * sizeof(uint32_t), s));
+  }
+  for (uint32_t g = 0; g < NG && n; g++) {
+    chk(cudaMemsetAsync(G[g].scalars, 0, 4 * sizeof(uint32_t), s));
+    chk(cudaMemsetAsync(G[g].hnt, 0, (G[g].max_tiles + 2) * sizeof(uint32_t), s));
+    chk(cudaMemsetAsync(G[g].tie, 0, (G[g].max_tiles + 2) * sizeof(uint32_t), s));
+    if (g > 0) chk(cudaMemsetAsync(G[g].Cseg, 0, G[g].max_rows * (G[g].ndig + 1) * sizeof(uint32_t), s));
+  }
+
+  // ---- A1: validate + chunked digit histogram of the top tau0 bits ----
   {
-    const uint32_t shift = L - Lh;
-    const size_t smem = (pair16 ? nbins / 2 : nbins) * sizeof(uint32_t);
+    const uint32_t tau0 = NG ? G[0].tau : 0;
+    const uint32_t shift = L - tau0;
     rec.begin("k_hist", n * eb);
-#define HIST_LAUNCH(T, PAIR)                                                                          \
-  do {                                                                                                \
-    cudaFuncSetAttribute(k_hist<T, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
-    k_hist<T, PAIR><<<hist_ctas, 1024, smem, s>>>((const T *)seq, n, sigma, shift, nbins, partial, adj, \
-                                                   err);                                              \
-  } while (0)
-    if (eb == 1) HIST_LAUNCH(uint8_t, false);
-    else if (eb == 2) { if (pair16) HIST_LAUNCH(uint16_t, true); else HIST_LAUNCH(uint16_t, false); }
-    else { if (pair16) HIST_LAUNCH(uint32_t, true); else HIST_LAUNCH(uint32_t, false); }
-#undef HIST_LAUNCH
-    chk(cudaGetLastError());
-    rec.end();
-    rec.begin("k_hist_reduce", (uint64_t)hist_ctas * nbins * 4);
-    k_hist_reduce<<<(nbins + 255) / 256, 256, 0, s>>>(partial, hist_ctas, nbins, adj, hist);
-    chk(cudaGetLastError());
-    rec.end();
-    rec.begin("k_scan_hist", (uint64_t)nbins * 8);
-    k_scan_hist<<<1, 1024, 0, s>>>(hist, nbins, Hx, err);
+    if (eb == 1)
+      k_hist<uint8_t><<<K, 1024, 0, s>>>((const uint8_t *)seq, n, sigma, shift, 1u << tau0, CH, partial, err);
+    else if (eb == 2)
+      k_hist<uint16_t><<<K, 1024, 0, s>>>((const uint16_t *)seq, n, sigma, shift, 1u << tau0, CH, partial, err);
+    else
+      k_hist<uint32_t><<<K, 1024, 0, s>>>((const uint32_t *)seq, n, sigma, shift, 1u << tau0, CH, partial, err);
     chk(cudaGetLastError());
     rec.end();
   }
 
   if (L > 0 && n > 0) {
-    // ---- A4: node table ----
-    rec.begin("k_node_count", 0);
-    k_node_count<<<L, 1024, 0, s>>>(Hx, Lh, ncount, err);
-    chk(cudaGetLastError());
-    rec.end();
-    rec.begin("k_node_emit", max_nodes * 8);
-    k_node_emit<<<L, 1024, 0, s>>>(Hx, Lh, L, ncount, t->level_node_ptr, t->node_key, t->node_start, err);
-    chk(cudaGetLastError());
-    rec.end();
-
-    // ---- group 0: levels 0..tau0-1 over S ----
-    GroupParams gp{};
-    gp.keys_in = seq;
-    gp.keys_out = keys1;
-    gp.n = n;
-    gp.Lh = Lh;
-    gp.l0 = 0;
-    gp.tau = tau0;
-    gp.pbits = L - tau0;
-    gp.Hx = Hx;
-    gp.single_seg = 1;
-    gp.ntiles_single = (uint32_t)max_tiles0;
-    gp.level_node_ptr = t->level_node_ptr;
-    gp.node_key = t->node_key;
-    gp.node_start = t->node_start;
-    gp.tile_counter = counters;
-    gp.state = state;
-    gp.bits = t->bits;
-    gp.wpl = WPL;
-    gp.blkcnt = blkcnt;
-    gp.bpl = BPL;
-    gp.err = err;
-    const uint64_t g0_bytes = n * eb + (tau1 ? n : 0) + (uint64_t)tau0 * n / 8;
-    rec.begin("k_group0", g0_bytes);
-    if (tau1 == 0) {
-      if (eb == 1) chk(launch_group<uint8_t, uint8_t, false>(gp, s, group_grid<uint8_t>()));
-      else if (eb == 2) chk(launch_group<uint16_t, uint8_t, false>(gp, s, group_grid<uint8_t>()));
-      else chk(launch_group<uint32_t, uint8_t, false>(gp, s, group_grid<uint8_t>()));
-    } else {
-      if (eb == 2) chk(launch_group<uint16_t, uint16_t, true>(gp, s, group_grid<uint16_t>()));
-      else chk(launch_group<uint32_t, uint16_t, true>(gp, s, group_grid<uint16_t>()));
-    }
-    rec.end();
-
-    if (tau1) {
-      // ---- group 1: levels tau0..L-1 over the narrowed keys, per level-tau0 node ----
-      rec.begin("k_segments", 0);
-      k_segments<<<1, 1024, 0, s>>>(t->level_node_ptr, tau0, t->node_start, n, seg_tile_base, tile_seg,
-                                    total_tiles, err);
+    for (uint32_t g = 0; g < NG; g++) {
+      GroupBufs &gb = G[g];
+      // ---- chains + digit table (Cseg) of this group ----
+      if (g == 0) {
+        rec.begin("k_chunk_scan", (uint64_t)K * gb.ndig * 8);
+        k_chunk_scan<<<1, NDIG, 0, s>>>(partial, K, gb.ndig, n, CH, gb.chain_prefix, gb.Cseg, gb.row_start,
+                                        gb.chain_begin, gb.chain_end, gb.chain_key, gb.chain_row, gb.scalars, err);
+        chk(cudaGetLastError());
+        rec.end();
+        chk(cudaMemsetAsync(gb.scalars + 3, 0, sizeof(uint32_t), s));
+        static const uint32_t one = 1;
+        chk(cudaMemcpyAsync(gb.scalars + 3, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+      } else {
+        rec.begin("k_chains", gb.max_chains * 24);
+        k_chains_from_nodes<<<(unsigned)std::min<uint64_t>((gb.max_chains + 255) / 256, 4096), 256, 0, s>>>(
+            t->level_node_ptr, ncount, gb.l0, t->node_key, t->node_start, n, gb.chain_begin, gb.chain_end, gb.chain_key,
+            gb.chain_row, gb.row_start, gb.scalars, err);
+        chk(cudaGetLastError());
+        rec.end();
+        chk(cudaMemcpyAsync(gb.scalars + 3, gb.scalars, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+      }
+      // ---- claim order ----
+      rec.begin("k_claims", gb.max_tiles * 8);
+      k_claims<<<1, 1024, 0, s>>>(gb.chain_begin, gb.chain_end, gb.scalars, gb.tile_base, gb.hnt, gb.cum, gb.tie,
+                                  gb.claim, gb.scalars + 1, err);
       chk(cudaGetLastError());
       rec.end();
-      chk(cudaMemsetAsync(state, 0, max_tiles1 * NDIG * sizeof(uint32_t), s));
-      GroupParams g1 = gp;
-      g1.keys_in = keys1;
-      g1.keys_out = nullptr;
-      g1.l0 = tau0;
-      g1.tau = tau1;
-      g1.pbits = 0;
-      g1.single_seg = 0;
-      g1.tile_seg = tile_seg;
-      g1.seg_tile_base = seg_tile_base;
-      g1.total_tiles = total_tiles;
-      g1.tile_counter = counters + 1;
-      rec.begin("k_group1", n + (uint64_t)tau1 * n / 8);
-      chk(launch_group<uint8_t, uint8_t, false>(g1, s, group_grid<uint8_t>()));
+      if (g > 0) {
+        // per-row digit histogram of the narrowed keys -> Cseg
+        rec.begin("k_seg_hist", n);
+        k_seg_hist<uint8_t><<<num_sms() * 8, 256, 0, s>>>((const uint8_t *)keys1, gb.pbits, gb.ndig, gb.claim,
+                                                          gb.scalars + 1, gb.chain_begin, gb.chain_end,
+                                                          gb.chain_row, gb.Cseg, err);
+        chk(cudaGetLastError());
+        rec.end();
+        rec.begin("k_seg_scan", gb.max_rows * (gb.ndig + 1) * 8);
+        k_seg_scan<<<(unsigned)((gb.max_rows * 32 + 255) / 256), 256, 0, s>>>(gb.Cseg, gb.scalars + 3, gb.ndig, err);
+        chk(cudaGetLastError());
+        rec.end();
+      }
+      // ---- A4: node table of this group's levels ----
+      {
+        const uint32_t k_lo = g == 0 ? 0u : 1u;
+        const uint32_t k_hi = std::min<uint32_t>(gb.tau, L - 1 - gb.l0);  // inclusive
+        if (k_hi >= k_lo) {
+          rec.begin("k_nodes_count", 0);
+          k_nodes_count<<<k_hi - k_lo + 1, 1024, 0, s>>>(gb.Cseg, gb.scalars + 3, gb.tau, gb.l0, k_lo, ncount, err);
+          chk(cudaGetLastError());
+          rec.end();
+          rec.begin("k_nodes_emit", 0);
+          k_nodes_emit<<<k_hi - k_lo + 1, 1024, 0, s>>>(gb.Cseg, gb.scalars + 3, gb.tau, gb.l0, k_lo, L,
+                                                        gb.chain_key, gb.row_start, ncount, t->level_node_ptr,
+                                                        t->node_key, t->node_start, err);
+          chk(cudaGetLastError());
+          rec.end();
+        }
+      }
+      // ---- the fused tau-level pass ----
+      if (g > 0) chk(cudaMemsetAsync(state, 0, gb.max_tiles * NDIG * sizeof(uint32_t), s));
+      else chk(cudaMemsetAsync(state, 0, max_tiles * NDIG * sizeof(uint32_t), s));
+      GroupParams gp{};
+      gp.keys_in = g == 0 ? seq : keys1;
+      gp.keys_out = (g + 1 < NG) ? keys1 : nullptr;
+      gp.n = n;
+      gp.l0 = gb.l0;
+      gp.tau = gb.tau;
+      gp.pbits = gb.pbits;
+      gp.claim = gb.claim;
+      gp.total_tiles = gb.scalars + 1;
+      gp.tile_base = gb.tile_base;
+      gp.chain_begin = gb.chain_begin;
+      gp.chain_end = gb.chain_end;
+      gp.chain_key = gb.chain_key;
+      gp.chain_row = gb.chain_row;
+      gp.chain_prefix = gb.chain_prefix;
+      gp.Cseg = gb.Cseg;
+      gp.row_start = gb.row_start;
+      gp.tile_counter = gb.scalars + 2;
+      gp.state = state;
+      gp.bits = t->bits;
+      gp.wpl = WPL;
+      gp.blkcnt = blkcnt;
+      gp.bpl = BPL;
+      gp.err = err;
+      const bool has_out = g + 1 < NG;
+      const uint64_t in_bytes = g == 0 ? n * eb : n;
+      char name[32];
+      snprintf(name, sizeof(name), "k_group%u", g);
+      rec.begin(name, in_bytes + (has_out ? n : 0) + (uint64_t)gb.tau * n / 8);
+      if (g > 0) {
+        chk(launch_group<uint8_t, uint8_t, uint8_t, false>(gp, s));
+      } else if (!has_out) {
+        if (eb == 1) chk(launch_group<uint8_t, uint8_t, uint8_t, false>(gp, s));
+        else if (eb == 2) chk(launch_group<uint16_t, uint8_t, uint8_t, false>(gp, s));
+        else chk(launch_group<uint32_t, uint8_t, uint8_t, false>(gp, s));
+      } else {
+        if (eb == 2) chk(launch_group<uint16_t, uint16_t, uint8_t, true>(gp, s));
+        else chk(launch_group<uint32_t, uint16_t, uint8_t, true>(gp, s));
+      }
       rec.end();
     }
 
@@ -372,8 +433,8 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     if (NSD) {
       const uint64_t warps = (uint64_t)L * NSD;
       rec.begin("k_rank_local", L * BPL * 6 + L * NSD * 8);
-      k_rank_local<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(blkcnt, BPL, NSD, L, t->rank_block,
-                                                                        suptot, err);
+      k_rank_local<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(blkcnt, BPL, NSD, L, t->rank_block, suptot,
+                                                                        err);
       chk(cudaGetLastError());
       rec.end();
     }
@@ -386,7 +447,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     chk(cudaMemsetAsync(t->rank_super, 0, L * SPL * sizeof(uint64_t), s));
   }
 
-  // ---- the single host sync: error flag + node counts ----
+  // ---- the single host sync: error flag + node count ----
   chk(cudaMemcpyAsync(h_stage, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   if (L) chk(cudaMemcpyAsync(h_stage + 1, t->level_node_ptr + L, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   A.free_scratch();

@@ -20,7 +20,7 @@ for ci in cfgs:
         t.free()
     prof = wt.last_profile()
     nl = cfg.n * cfg.levels
-    print(f"cfg{ci}: build {ms:.3f} ms  {nl/ms/1e6:.3e} sym-levels/s  launches={prof['total_launches']}")
+    print(f"cfg{ci}: build {ms:.3f} ms  {nl/(ms*1e-3):.3e} sym-levels/s  launches={prof['total_launches']}")
     for k in prof["kernels"]:
         bw = k["algo_bytes"] / (k["ms"] * 1e-3) / 1e9 if k["ms"] > 0 else 0
         print(f"   {k['name']:16s} {k['ms']:8.3f} ms x{k['launches']}  algo {k['algo_bytes']/1e6:9.1f} MB  {bw:8.1f} GB/s")
