@@ -48,29 +48,57 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """SM clock and throttle-reason sampling during the timed region (NVML,
+    every 20 ms; the nvidia-smi query of B200_PROFILING.md as a fallback)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_s: float = 0.02):
         self.idx = gpu_index
-        self.rows = []
+        self.period = period_s
+        self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)))
+        self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for name, bit in self.REASONS.items():
+            if r & bit:
+                self.reasons.add(name)
+
+    def _sample_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        if out:
+            f = [x.strip() for x in out.split(",")]
+            self.sm.append(float(f[0]))
+            self.mx.append(float(f[1]))
+            for nm, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], f[2:6]):
+                if v.lower() == "active":
+                    self.reasons.add(nm)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self._sample_nvml() if self._nvml else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -82,18 +110,22 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for nm, v in zip(names, r[5:9]):
-                if v.strip().lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx),
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
+
+
+def aggregate(ms_local: float, units_per_rank: int, world: int, dist=None, device=None):
+    """Max-over-ranks step time and whole-job throughput (units of all ranks)."""
+    ms = ms_local
+    if world > 1 and dist is not None:
+        import torch
+        t = torch.tensor([ms_local], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, units_per_rank * world / (ms / 1e3)
 
 
 def cpu_model():
@@ -106,12 +138,13 @@ def cpu_model():
     return "unknown"
 
 
-def run_oracle_sample(cfg, n_sample: int, repeats: int = 1):
+def run_oracle_sample(cfg, n_sample: int, repeats: int = 1, S=None):
     """Time the single-threaded C oracle (as it stands) on the first n_sample
     symbols of the config's stream; returns (symbol-levels/s, seconds, n)."""
     import gen
     import oracle
-    S = gen.config_input(cfg, n_sample)
+    if S is None:
+        S = gen.config_input(cfg, n_sample)
     times = []
     for _ in range(repeats):
         t0 = time.perf_counter()
@@ -125,7 +158,7 @@ def run_oracle_sample(cfg, n_sample: int, repeats: int = 1):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -149,12 +182,13 @@ def main():
         if rank != 0:
             return
         n_s = 1 << args.cpu_sample_log2
+        S_sample = gen.config_input(cfg, n_s)
         for _ in range(args.warmup):
-            run_oracle_sample(cfg, min(n_s, 1 << 16))
+            run_oracle_sample(cfg, 1 << 16, S=S_sample[:1 << 16])
         t0 = time.perf_counter()
         tot = 0.0
         for _ in range(args.steps):
-            v, t, _n = run_oracle_sample(cfg, n_s)
+            v, t, _n = run_oracle_sample(cfg, n_s, S=S_sample)
             tot += t
         ms = tot / args.steps * 1e3
         value = n_s * cfg.levels / (ms / 1e3)
@@ -224,12 +258,7 @@ def main():
     barrier()
     wt.profile_enable(False)
     ms_local = e0.elapsed_time(e1) / args.steps
-    ms = ms_local
-    if world > 1:
-        tt = torch.tensor([ms_local], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    value = units * world / (ms / 1e3)
+    ms, value = aggregate(ms_local, units, world, dist if world > 1 else None, torch.device("cuda"))
 
     # ---- end to end through the C ABI with host buffers ----
     e2e = None
@@ -244,12 +273,9 @@ def main():
             wt.build_host(S_pinned, cfg.sigma, stream).free()
         t1.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = t0.elapsed_time(t1) / args.steps
-        if world > 1:
-            tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_ms = float(tt.item())
-        e2e = {"value": units * world / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+        e2e_ms, e2e_val = aggregate(t0.elapsed_time(t1) / args.steps, units, world,
+                                    dist if world > 1 else None, torch.device("cuda"))
+        e2e = {"value": e2e_val, "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": cfg.n * cfg.elem_bytes,
                "d2h_bytes_per_step": 12}  # error flag (u32) + total node count (u64)
 

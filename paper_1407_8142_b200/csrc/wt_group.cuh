@@ -62,13 +62,11 @@ struct WarpSmem {
   uint32_t hist[NDIG];           // digit counts; then before[]; then key bases
   uint32_t Hl[NDIG + 1];         // exclusive scan of hist (local group starts)
   uint32_t BX[NDIG + 1];         // exclusive scan of before[]
-  uint32_t T[NDIG];              // split table of the current level (2^(k+1) entries)
+  uint16_t T[NDIG];              // split table of the current level (2^(k+1) entries)
   uint32_t RG[NDIG / 2 + 1];     // run global start
-  uint32_t RL[NDIG / 2 + 1];     // run local start
-  uint32_t RC[NDIG / 2 + 1];     // run length
 };
 
-constexpr int GROUP_WARPS = 4;
+constexpr int GROUP_WARPS = 2;
 constexpr int U = 8;  // chunks per software-pipelined batch
 
 // Write the bits of one run [G, G+cnt) <- local bits [ls, ls+cnt) of LB
@@ -259,16 +257,15 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32) k_group(GroupParams p) {
         for (uint32_t q = lo; q < hi; q++) {
           const uint32_t gs = ws.Hl[q << sh], ge = ws.Hl[(q + 1) << sh];
           const uint32_t ones = ws.Hl[(2 * q + 2) << (sh - 1)] - ws.Hl[(2 * q + 1) << (sh - 1)];
-          ws.T[2 * q] = O;                    // O(gs)
-          ws.T[2 * q + 1] = ge - (O + ones);  // ge - O(ge)
+          ws.T[2 * q] = (uint16_t)O;                    // O(gs)
+          ws.T[2 * q + 1] = (uint16_t)(ge - (O + ones));  // ge - O(ge)
           O += ones;
-          ws.RL[q] = gs;
-          ws.RC[q] = ge - gs;
+          (void)gs;
           ws.RG[q] = rstart + Crow[q << sh] + (ws.BX[(q + 1) << sh] - ws.BX[q << sh]);
         }
       }
       __syncwarp();
-      const uint32_t *__restrict__ Tk = ws.T;
+      const uint16_t *__restrict__ Tk = ws.T;
       uint32_t Orun = 0;
       const uint32_t full = len / (32 * U);
       for (uint32_t b = 0; b < full; b++) {
@@ -284,12 +281,25 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32) k_group(GroupParams p) {
             m[u] = __ballot_sync(FULL, tag & 1u);
             tb[u] = Tk[tag];
           }
+          uint32_t pc[U], ob[U];
+#pragma unroll
+          for (int u = 0; u < U; u++) pc[u] = __popc(m[u]);
+          // ones before chunk u of the batch: short dependency tree, not a chain
+          ob[0] = Orun;
+          ob[1] = Orun + pc[0];
+          const uint32_t p01 = pc[0] + pc[1], p23 = pc[2] + pc[3], p45 = pc[4] + pc[5];
+          ob[2] = Orun + p01;
+          ob[3] = ob[2] + pc[2];
+          ob[4] = ob[2] + p23;
+          ob[5] = ob[4] + pc[4];
+          ob[6] = ob[4] + p45;
+          ob[7] = ob[6] + pc[6];
+          Orun = ob[7] + pc[7];
 #pragma unroll
           for (int u = 0; u < U; u++) {
-            const uint32_t Y = Orun + __popc(m[u] & lt);
+            const uint32_t Y = ob[u] + __popc(m[u] & lt);
             const uint32_t d = ((r[u] >> bitsh) & 1u) ? tb[u] + Y : tb[u] + (cbase + u * 32) - Y;
             dst[d] = (RecT)r[u];
-            Orun += __popc(m[u]);
           }
         } else {
 #pragma unroll
@@ -322,15 +332,15 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32) k_group(GroupParams p) {
       uint32_t *BC = p.blkcnt + (uint64_t)(p.l0 + k) * p.bpl;
       if (nq >= 32) {
         for (uint32_t q = lane; q < nq; q += 32) {  // one lane per run
-          const uint32_t cnt = ws.RC[q];
+          const uint32_t ls = ws.Hl[q << sh], cnt = ws.Hl[(q + 1) << sh] - ls;
           if (cnt) {
             const uint32_t G = ws.RG[q];
-            put_run_words(ws.LB, B, BC, p.n, G, ws.RL[q], cnt, G >> 6, (((uint64_t)G + cnt - 1) >> 6) + 1);
+            put_run_words(ws.LB, B, BC, p.n, G, ls, cnt, G >> 6, (((uint64_t)G + cnt - 1) >> 6) + 1);
           }
         }
       } else {
         for (uint32_t q = 0; q < nq; q++) {  // lanes split a run's words
-          const uint32_t cnt = ws.RC[q];
+          const uint32_t ls = ws.Hl[q << sh], cnt = ws.Hl[(q + 1) << sh] - ls;
           if (!cnt) continue;
           const uint32_t G = ws.RG[q];
           const uint64_t w0 = G >> 6, w1 = (((uint64_t)G + cnt - 1) >> 6) + 1;
@@ -340,7 +350,7 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32) k_group(GroupParams p) {
           uint64_t a = w0 + lane * per, e = a + per;
           if (a > w1) a = w1;
           if (e > w1) e = w1;
-          if (a < e) put_run_words(ws.LB, B, BC, p.n, G, ws.RL[q], cnt, a, e);
+          if (a < e) put_run_words(ws.LB, B, BC, p.n, G, ls, cnt, a, e);
         }
       }
       __syncwarp();
@@ -353,11 +363,19 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32) k_group(GroupParams p) {
       for (uint32_t d = lane; d < ndig; d += 32)
         ws.hist[d] = rstart + Crow[d] + ws.hist[d] - ws.Hl[d];  // key base per digit
       __syncwarp();
-      for (uint32_t c = 0; c < nch; c++) {
-        const uint32_t pos = c * 32 + lane;
-        if (pos < len) {
-          const uint32_t r = fin[pos];
-          ko[ws.hist[r >> pbits] + pos] = (OutT)(r & pmask);
+      for (uint32_t c0 = 0; c0 < nch; c0 += U) {
+        uint32_t r[U], kb[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const uint32_t pos = (c0 + u) * 32 + lane;
+          r[u] = pos < len ? (uint32_t)fin[pos] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) kb[u] = ws.hist[r[u] >> pbits];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const uint32_t pos = (c0 + u) * 32 + lane;
+          if (pos < len) ko[kb[u] + pos] = (OutT)(r[u] & pmask);
         }
       }
       __syncwarp();

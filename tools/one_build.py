@@ -6,7 +6,7 @@ import gen
 import paper_1407_8142_b200 as wt
 
 ci = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-n = int(sys.argv[2]) if len(sys.argv) > 2 else None
+n = (int(sys.argv[2]) or None) if len(sys.argv) > 2 else None
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 cfg = gen.CONFIGS[ci]
 S = torch.from_numpy(gen.config_input(cfg, n)).cuda()
