@@ -78,8 +78,7 @@ typedef struct wt_tree {
  *   d_seq      DEVICE pointer to n symbols of elem_bytes bytes each
  *              (little-endian unsigned).  Caller-owned, read-only, not
  *              retained after return.  Any alignment is accepted.
- *   n          sequence length; 0 <= n < 2^30 in this build (larger n
- *              returns WT_EUNSUPPORTED).
+ *   n          sequence length, 0 <= n < 2^32.
  *   elem_bytes 1, 2 or 4.
  *   sigma      alphabet size, 1 <= sigma <= 2^(8*elem_bytes); this build
  *              supports L = ceil(log2 sigma) <= 16 (larger: WT_EUNSUPPORTED).

@@ -6,7 +6,10 @@
 namespace wtb {
 
 constexpr uint32_t FULL = 0xffffffffu;
-constexpr int TW = 4096;                 // elements per warp tile
+#ifndef WT_TW
+#define WT_TW 4096
+#endif
+constexpr int TW = WT_TW;                // elements per warp tile
 constexpr int NCH = TW / 32;             // 32-element chunks per tile
 constexpr int TAU_MAX = 8;               // levels fused per HBM pass
 constexpr int NDIG = 1 << TAU_MAX;       // digit values per pass

@@ -151,42 +151,59 @@ struct Allocs {
   }
 };
 
+// Launch configuration of one k_group instantiation (persistent, occupancy-sized grid).
+struct GroupLaunch {
+  void (*kern)(GroupParams) = nullptr;
+  size_t smem = 0;
+  int grid = 0;
+};
+
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
-cudaError_t launch_group(const GroupParams &gp, cudaStream_t s) {
-  const size_t smem = GROUP_WARPS * sizeof(WarpSmem<RecT>);
-  auto kern = k_group<InT, RecT, OutT, HAS_OUT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GROUP_WARPS * 32, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  kern<<<num_sms() * per_sm, GROUP_WARPS * 32, smem, s>>>(gp);
-  return cudaGetLastError();
+GroupLaunch group_launch() {
+  static GroupLaunch gl;
+  static std::once_flag f;
+  std::call_once(f, [] {
+    gl.kern = k_group<InT, RecT, OutT, HAS_OUT>;
+    gl.smem = GROUP_WARPS * sizeof(WarpSmem<RecT>);
+    cudaFuncSetAttribute(gl.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gl.smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl.kern, GROUP_WARPS * 32, gl.smem);
+    gl.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
+  });
+  return gl;
 }
 
-// Per-group scratch: chains, claim order, digit tables.
+GroupLaunch pick_group(uint32_t g, uint32_t NG, uint32_t eb) {
+  const bool has_out = g + 1 < NG;
+  if (g > 0) return group_launch<uint8_t, uint8_t, uint8_t, false>();
+  if (!has_out) {
+    if (eb == 1) return group_launch<uint8_t, uint8_t, uint8_t, false>();
+    if (eb == 2) return group_launch<uint16_t, uint8_t, uint8_t, false>();
+    return group_launch<uint32_t, uint8_t, uint8_t, false>();
+  }
+  if (eb == 2) return group_launch<uint16_t, uint16_t, uint8_t, true>();
+  return group_launch<uint32_t, uint16_t, uint8_t, true>();
+}
+
+// Per-group scratch: chains, rows, digit tables.
 struct GroupBufs {
   uint32_t tau = 0, l0 = 0, pbits = 0, ndig = 0;
-  uint64_t max_chains = 0, max_tiles = 0, max_rows = 0;
-  uint32_t *chain_begin = nullptr, *chain_end = nullptr, *chain_key = nullptr, *chain_row = nullptr;
-  uint32_t *row_start = nullptr, *chain_prefix = nullptr, *tile_base = nullptr;
-  uint32_t *hnt = nullptr, *tie = nullptr, *cum = nullptr, *Cseg = nullptr;
-  uint32_t *scalars = nullptr;  // [0] nchains, [1] total tiles, [2] tile counter, [3] nrows
-  uint2 *claim = nullptr;
+  uint64_t CH = TW, max_chains = 0, max_rows = 0;
+  GroupLaunch gl;
+  uint32_t *chain_begin = nullptr, *chain_end = nullptr, *chain_row = nullptr;
+  uint32_t *row_first = nullptr, *row_start = nullptr, *row_key = nullptr;
+  uint32_t *E = nullptr, *Cseg = nullptr;
+  uint32_t *counts = nullptr;  // [0] chains, [1] rows, [2] chain claim counter
   void alloc(Allocs &A) {
     chain_begin = A.alloc<uint32_t>(max_chains, false);
     chain_end = A.alloc<uint32_t>(max_chains, false);
-    chain_key = A.alloc<uint32_t>(max_chains, false);
     chain_row = A.alloc<uint32_t>(max_chains, false);
+    row_first = A.alloc<uint32_t>(max_rows + 1, false);
     row_start = A.alloc<uint32_t>(max_rows, false);
-    tile_base = A.alloc<uint32_t>(max_chains, false);
-    hnt = A.alloc<uint32_t>(max_tiles + 2, false);
-    tie = A.alloc<uint32_t>(max_tiles + 2, false);
-    cum = A.alloc<uint32_t>(max_tiles + 2, false);
+    row_key = A.alloc<uint32_t>(max_rows, false);
+    E = A.alloc<uint32_t>((uint64_t)ndig * (max_chains + 1), false);
     Cseg = A.alloc<uint32_t>(max_rows * (ndig + 1), false);
-    scalars = A.alloc<uint32_t>(4, false);
-    claim = A.alloc<uint2>(max_tiles, false);
+    counts = A.alloc<uint32_t>(4, false);
   }
 };
 
@@ -199,7 +216,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   if (n >= (1ull << 32)) return WT_EINVAL;
   if (n > 0 && !(from_host ? h_seq : d_seq)) return WT_EINVAL;
   const uint32_t L = levels_of(sigma);
-  if (L > 16 || n >= (1ull << 30)) return WT_EUNSUPPORTED;
+  if (L > 16) return WT_EUNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream_v);
   configure_pool_once();
 
@@ -243,39 +260,32 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     seq = d;
   }
 
-  // ---- plan: groups of <= 8 levels; A1 chunks are the group-0 chains ----
+  // ---- plan: groups of <= 8 levels, chains sized to ~3 per resident warp ----
   const uint32_t NG = (L + TAU_MAX - 1) / TAU_MAX;
   GroupBufs G[2];
-  const uint64_t ntiles_n = std::max<uint64_t>((n + TW - 1) / TW, 1);
-  uint32_t K = (uint32_t)std::min<uint64_t>((uint64_t)num_sms() * 2, ntiles_n);
-  const uint64_t CH = ((ntiles_n + K - 1) / K) * TW;
-  K = (uint32_t)std::max<uint64_t>((n + CH - 1) / CH, 1);
   for (uint32_t g = 0; g < NG; g++) {
     GroupBufs &gb = G[g];
     gb.l0 = g * TAU_MAX;
     gb.tau = std::min<uint32_t>(TAU_MAX, L - gb.l0);
     gb.pbits = L - gb.l0 - gb.tau;
     gb.ndig = 1u << gb.tau;
+    gb.gl = pick_group(g, NG, eb);
+    const uint64_t warps = (uint64_t)gb.gl.grid * GROUP_WARPS;
+    static const uint64_t cpw = getenv("WT_CHAINS_PER_WARP") ? strtoull(getenv("WT_CHAINS_PER_WARP"), 0, 10) : 8;
+    const uint64_t target = (n + cpw * warps - 1) / (cpw * warps);
+    gb.CH = std::max<uint64_t>(TW, ((target + TW - 1) / TW) * TW);
     if (g == 0) {
-      gb.max_chains = K;
+      gb.max_chains = std::max<uint64_t>((n + gb.CH - 1) / gb.CH, 1);
       gb.max_rows = 1;
-      gb.max_tiles = ntiles_n + 1;
     } else {
-      gb.max_chains = std::min<uint64_t>(1ull << gb.l0, std::max<uint64_t>(n, 1));
-      gb.max_rows = gb.max_chains;
-      gb.max_tiles = ntiles_n + gb.max_chains + 1;
+      gb.max_rows = std::min<uint64_t>(1ull << gb.l0, std::max<uint64_t>(n, 1));
+      gb.max_chains = (n + gb.CH - 1) / gb.CH + gb.max_rows;
     }
     gb.alloc(A);
   }
   uint32_t *err = A.alloc<uint32_t>(4, false);
-  uint32_t *partial = A.alloc<uint32_t>((uint64_t)K * NDIG, false);
-  if (NG) G[0].chain_prefix = A.alloc<uint32_t>((uint64_t)K * NDIG, false);
   uint32_t *ncount = A.alloc<uint32_t>(L + 1, false);
-  uint32_t *blkcnt = A.alloc<uint32_t>(L * BPL, false);
   uint64_t *suptot = A.alloc<uint64_t>(L * NSD, false);
-  uint64_t max_tiles = 1;
-  for (uint32_t g = 0; g < NG; g++) max_tiles = std::max(max_tiles, G[g].max_tiles);
-  uint32_t *state = A.alloc<uint32_t>(max_tiles * NDIG, false);
   void *keys1 = NG > 1 ? (void *)A.alloc<uint8_t>(n, false) : nullptr;
 
   static uint64_t *h_stage = nullptr;  // pinned staging for the single D2H
@@ -300,141 +310,124 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
 
   chk(cudaMemsetAsync(err, 0, 4 * sizeof(uint32_t), s));
   chk(cudaMemsetAsync(t->level_node_ptr, 0, (L + 1) * sizeof(uint64_t), s));
-  if (L && n) {
-    chk(cudaMemsetAsync(t->bits, 0, L * WPL * sizeof(uint64_t), s));
-    chk(cudaMemsetAsync(blkcnt, 0, L * BPL * sizeof(uint32_t), s));
-  }
-  for (uint32_t g = 0; g < NG && n; g++) {
-    chk(cudaMemsetAsync(G[g].scalars, 0, 4 * sizeof(uint32_t), s));
-    chk(cudaMemsetAsync(G[g].hnt, 0, (G[g].max_tiles + 2) * sizeof(uint32_t), s));
-    chk(cudaMemsetAsync(G[g].tie, 0, (G[g].max_tiles + 2) * sizeof(uint32_t), s));
-    if (g > 0) chk(cudaMemsetAsync(G[g].Cseg, 0, G[g].max_rows * (G[g].ndig + 1) * sizeof(uint32_t), s));
-  }
+  if (L && n) chk(cudaMemsetAsync(t->bits, 0, L * WPL * sizeof(uint64_t), s));
+  for (uint32_t g = 0; g < NG; g++) chk(cudaMemsetAsync(G[g].counts, 0, 4 * sizeof(uint32_t), s));
 
-  // ---- A1: validate + chunked digit histogram of the top tau0 bits ----
-  {
-    const uint32_t tau0 = NG ? G[0].tau : 0;
-    const uint32_t shift = L - tau0;
-    rec.begin("k_hist", n * eb);
-    if (eb == 1)
-      k_hist<uint8_t><<<K, 1024, 0, s>>>((const uint8_t *)seq, n, sigma, shift, 1u << tau0, CH, partial, err);
-    else if (eb == 2)
-      k_hist<uint16_t><<<K, 1024, 0, s>>>((const uint16_t *)seq, n, sigma, shift, 1u << tau0, CH, partial, err);
-    else
-      k_hist<uint32_t><<<K, 1024, 0, s>>>((const uint32_t *)seq, n, sigma, shift, 1u << tau0, CH, partial, err);
+  for (uint32_t g = 0; g < NG || (g == 0 && L == 0); g++) {
+    // ---- chains of this group + their digit histograms (A1 for g = 0) ----
+    if (g == 0) {
+      const uint64_t CH0 = NG ? G[0].CH : std::max<uint64_t>(n, 1);
+      const uint32_t K = NG ? (uint32_t)G[0].max_chains : (uint32_t)((n + CH0 - 1) / CH0);
+      const uint32_t tau0 = NG ? G[0].tau : 0;
+      const uint32_t ndig0 = 1u << tau0;
+      uint32_t *cb, *ce_, *cr, *rf, *rs, *rk, *E, *cnt;
+      uint32_t stride;
+      if (NG) {
+        GroupBufs &gb = G[0];
+        cb = gb.chain_begin; ce_ = gb.chain_end; cr = gb.chain_row; rf = gb.row_first; rs = gb.row_start;
+        rk = gb.row_key; E = gb.E; cnt = gb.counts; stride = (uint32_t)gb.max_chains + 1;
+      } else {  // sigma == 1: validation only
+        cb = A.alloc<uint32_t>(K, false); ce_ = A.alloc<uint32_t>(K, false); cr = A.alloc<uint32_t>(K, false);
+        rf = A.alloc<uint32_t>(2, false); rs = A.alloc<uint32_t>(1, false); rk = A.alloc<uint32_t>(1, false);
+        E = A.alloc<uint32_t>(K + 1, false); cnt = A.alloc<uint32_t>(4, false); stride = K + 1;
+        if (A.fail) { ce = cudaErrorMemoryAllocation; break; }
+      }
+      if (n) {
+        k_chains_root<<<(K + 255) / 256, 256, 0, s>>>(n, CH0, K, cb, ce_, cr, rf, rs, rk, cnt, err);
+        chk(cudaGetLastError());
+        rec.begin("k_hist", n * eb);
+        const uint32_t shift = L - tau0;
+        if (eb == 1)
+          k_chain_hist<uint8_t, true><<<std::min<uint32_t>(K, 4 * num_sms()), 512, 0, s>>>((const uint8_t *)seq, sigma, shift, ndig0, cb, ce_, cnt, stride, E, err);
+        else if (eb == 2)
+          k_chain_hist<uint16_t, true><<<std::min<uint32_t>(K, 4 * num_sms()), 512, 0, s>>>((const uint16_t *)seq, sigma, shift, ndig0, cb, ce_, cnt, stride, E, err);
+        else
+          k_chain_hist<uint32_t, true><<<std::min<uint32_t>(K, 4 * num_sms()), 512, 0, s>>>((const uint32_t *)seq, sigma, shift, ndig0, cb, ce_, cnt, stride, E, err);
+        chk(cudaGetLastError());
+        rec.end();
+      }
+      if (!NG || !n) break;
+    } else {
+      GroupBufs &gb = G[g];
+      rec.begin("k_chains", gb.max_chains * 12);
+      k_chains_from_nodes<<<1, 1024, 0, s>>>(t->level_node_ptr, ncount, gb.l0, t->node_key, t->node_start, n,
+                                             gb.CH, gb.chain_begin, gb.chain_end, gb.chain_row, gb.row_first,
+                                             gb.row_start, gb.row_key, gb.counts, err);
+      chk(cudaGetLastError());
+      rec.end();
+      rec.begin("k_seg_hist", n);
+      k_chain_hist<uint8_t, false><<<(unsigned)std::min<uint64_t>(gb.max_chains, 4 * num_sms()), 512, 0, s>>>(
+          (const uint8_t *)keys1, sigma, gb.pbits, gb.ndig, gb.chain_begin, gb.chain_end, gb.counts,
+          (uint32_t)gb.max_chains + 1, gb.E, err);
+      chk(cudaGetLastError());
+      rec.end();
+    }
+    GroupBufs &gb = G[g];
+    const uint32_t stride = (uint32_t)gb.max_chains + 1;
+    rec.begin("k_chain_scan", (uint64_t)gb.ndig * gb.max_chains * 8);
+    k_chain_scan<<<gb.ndig, 1024, 0, s>>>(gb.E, stride, gb.counts, err);
+    chk(cudaGetLastError());
+    rec.end();
+    rec.begin("k_row_scan", gb.max_rows * (gb.ndig + 1) * 4);
+    k_row_scan<<<(unsigned)((gb.max_rows * 32 + 255) / 256), 256, 0, s>>>(gb.E, stride, gb.row_first, gb.counts,
+                                                                          gb.ndig, gb.Cseg, err);
+    chk(cudaGetLastError());
+    rec.end();
+    // ---- A4: node table of this group's levels ----
+    {
+      const uint32_t k_lo = g == 0 ? 0u : 1u;
+      const uint32_t k_hi = std::min<uint32_t>(gb.tau, L - 1 - gb.l0);  // inclusive
+      if (k_hi >= k_lo) {
+        rec.begin("k_nodes_count", 0);
+        k_nodes_count<<<k_hi - k_lo + 1, 1024, 0, s>>>(gb.Cseg, gb.counts, gb.tau, gb.l0, k_lo, ncount, err);
+        chk(cudaGetLastError());
+        rec.end();
+        rec.begin("k_nodes_emit", 0);
+        k_nodes_emit<<<k_hi - k_lo + 1, 1024, 0, s>>>(gb.Cseg, gb.counts, gb.tau, gb.l0, k_lo, L, gb.row_key,
+                                                      gb.row_start, ncount, t->level_node_ptr, t->node_key,
+                                                      t->node_start, err);
+        chk(cudaGetLastError());
+        rec.end();
+      }
+    }
+    // ---- the fused tau-level pass ----
+    GroupParams gp{};
+    gp.keys_in = g == 0 ? seq : keys1;
+    gp.keys_out = (g + 1 < NG) ? keys1 : nullptr;
+    gp.n = n;
+    gp.l0 = gb.l0;
+    gp.tau = gb.tau;
+    gp.pbits = gb.pbits;
+    gp.counts = gb.counts;
+    gp.chain_begin = gb.chain_begin;
+    gp.chain_end = gb.chain_end;
+    gp.chain_row = gb.chain_row;
+    gp.row_first = gb.row_first;
+    gp.E = gb.E;
+    gp.estride = stride;
+    gp.Cseg = gb.Cseg;
+    gp.row_start = gb.row_start;
+    gp.chain_counter = gb.counts + 2;
+    gp.bits = t->bits;
+    gp.wpl = WPL;
+    gp.err = err;
+    const bool has_out = g + 1 < NG;
+    const uint64_t in_bytes = g == 0 ? n * eb : n;
+    char name[32];
+    snprintf(name, sizeof(name), "k_group%u", g);
+    rec.begin(name, in_bytes + (has_out ? n : 0) + (uint64_t)gb.tau * n / 8);
+    gb.gl.kern<<<gb.gl.grid, GROUP_WARPS * 32, gb.gl.smem, s>>>(gp);
     chk(cudaGetLastError());
     rec.end();
   }
 
   if (L > 0 && n > 0) {
-    for (uint32_t g = 0; g < NG; g++) {
-      GroupBufs &gb = G[g];
-      // ---- chains + digit table (Cseg) of this group ----
-      if (g == 0) {
-        rec.begin("k_chunk_scan", (uint64_t)K * gb.ndig * 8);
-        k_chunk_scan<<<1, NDIG, 0, s>>>(partial, K, gb.ndig, n, CH, gb.chain_prefix, gb.Cseg, gb.row_start,
-                                        gb.chain_begin, gb.chain_end, gb.chain_key, gb.chain_row, gb.scalars, err);
-        chk(cudaGetLastError());
-        rec.end();
-        chk(cudaMemsetAsync(gb.scalars + 3, 0, sizeof(uint32_t), s));
-        static const uint32_t one = 1;
-        chk(cudaMemcpyAsync(gb.scalars + 3, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-      } else {
-        rec.begin("k_chains", gb.max_chains * 24);
-        k_chains_from_nodes<<<(unsigned)std::min<uint64_t>((gb.max_chains + 255) / 256, 4096), 256, 0, s>>>(
-            t->level_node_ptr, ncount, gb.l0, t->node_key, t->node_start, n, gb.chain_begin, gb.chain_end, gb.chain_key,
-            gb.chain_row, gb.row_start, gb.scalars, err);
-        chk(cudaGetLastError());
-        rec.end();
-        chk(cudaMemcpyAsync(gb.scalars + 3, gb.scalars, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-      }
-      // ---- claim order ----
-      rec.begin("k_claims", gb.max_tiles * 8);
-      k_claims<<<1, 1024, 0, s>>>(gb.chain_begin, gb.chain_end, gb.scalars, gb.tile_base, gb.hnt, gb.cum, gb.tie,
-                                  gb.claim, gb.scalars + 1, err);
-      chk(cudaGetLastError());
-      rec.end();
-      if (g > 0) {
-        // per-row digit histogram of the narrowed keys -> Cseg
-        rec.begin("k_seg_hist", n);
-        k_seg_hist<uint8_t><<<num_sms() * 8, 256, 0, s>>>((const uint8_t *)keys1, gb.pbits, gb.ndig, gb.claim,
-                                                          gb.scalars + 1, gb.chain_begin, gb.chain_end,
-                                                          gb.chain_row, gb.Cseg, err);
-        chk(cudaGetLastError());
-        rec.end();
-        rec.begin("k_seg_scan", gb.max_rows * (gb.ndig + 1) * 8);
-        k_seg_scan<<<(unsigned)((gb.max_rows * 32 + 255) / 256), 256, 0, s>>>(gb.Cseg, gb.scalars + 3, gb.ndig, err);
-        chk(cudaGetLastError());
-        rec.end();
-      }
-      // ---- A4: node table of this group's levels ----
-      {
-        const uint32_t k_lo = g == 0 ? 0u : 1u;
-        const uint32_t k_hi = std::min<uint32_t>(gb.tau, L - 1 - gb.l0);  // inclusive
-        if (k_hi >= k_lo) {
-          rec.begin("k_nodes_count", 0);
-          k_nodes_count<<<k_hi - k_lo + 1, 1024, 0, s>>>(gb.Cseg, gb.scalars + 3, gb.tau, gb.l0, k_lo, ncount, err);
-          chk(cudaGetLastError());
-          rec.end();
-          rec.begin("k_nodes_emit", 0);
-          k_nodes_emit<<<k_hi - k_lo + 1, 1024, 0, s>>>(gb.Cseg, gb.scalars + 3, gb.tau, gb.l0, k_lo, L,
-                                                        gb.chain_key, gb.row_start, ncount, t->level_node_ptr,
-                                                        t->node_key, t->node_start, err);
-          chk(cudaGetLastError());
-          rec.end();
-        }
-      }
-      // ---- the fused tau-level pass ----
-      if (g > 0) chk(cudaMemsetAsync(state, 0, gb.max_tiles * NDIG * sizeof(uint32_t), s));
-      else chk(cudaMemsetAsync(state, 0, max_tiles * NDIG * sizeof(uint32_t), s));
-      GroupParams gp{};
-      gp.keys_in = g == 0 ? seq : keys1;
-      gp.keys_out = (g + 1 < NG) ? keys1 : nullptr;
-      gp.n = n;
-      gp.l0 = gb.l0;
-      gp.tau = gb.tau;
-      gp.pbits = gb.pbits;
-      gp.claim = gb.claim;
-      gp.total_tiles = gb.scalars + 1;
-      gp.tile_base = gb.tile_base;
-      gp.chain_begin = gb.chain_begin;
-      gp.chain_end = gb.chain_end;
-      gp.chain_key = gb.chain_key;
-      gp.chain_row = gb.chain_row;
-      gp.chain_prefix = gb.chain_prefix;
-      gp.Cseg = gb.Cseg;
-      gp.row_start = gb.row_start;
-      gp.tile_counter = gb.scalars + 2;
-      gp.state = state;
-      gp.bits = t->bits;
-      gp.wpl = WPL;
-      gp.blkcnt = blkcnt;
-      gp.bpl = BPL;
-      gp.err = err;
-      const bool has_out = g + 1 < NG;
-      const uint64_t in_bytes = g == 0 ? n * eb : n;
-      char name[32];
-      snprintf(name, sizeof(name), "k_group%u", g);
-      rec.begin(name, in_bytes + (has_out ? n : 0) + (uint64_t)gb.tau * n / 8);
-      if (g > 0) {
-        chk(launch_group<uint8_t, uint8_t, uint8_t, false>(gp, s));
-      } else if (!has_out) {
-        if (eb == 1) chk(launch_group<uint8_t, uint8_t, uint8_t, false>(gp, s));
-        else if (eb == 2) chk(launch_group<uint16_t, uint8_t, uint8_t, false>(gp, s));
-        else chk(launch_group<uint32_t, uint8_t, uint8_t, false>(gp, s));
-      } else {
-        if (eb == 2) chk(launch_group<uint16_t, uint16_t, uint8_t, true>(gp, s));
-        else chk(launch_group<uint32_t, uint16_t, uint8_t, true>(gp, s));
-      }
-      rec.end();
-    }
-
-    // ---- A7 finalize ----
+    // ---- A7: rank directory from the finished bitmaps ----
     if (NSD) {
       const uint64_t warps = (uint64_t)L * NSD;
-      rec.begin("k_rank_local", L * BPL * 6 + L * NSD * 8);
-      k_rank_local<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(blkcnt, BPL, NSD, L, t->rank_block, suptot,
-                                                                        err);
+      rec.begin("k_rank_local", L * WPL * 8 + L * BPL * 2 + L * NSD * 8);
+      k_rank_local<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(t->bits, WPL, BPL, NSD, L, t->rank_block,
+                                                                        suptot, err);
       chk(cudaGetLastError());
       rec.end();
     }

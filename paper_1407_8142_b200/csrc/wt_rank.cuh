@@ -2,8 +2,8 @@
 //
 // Directory (reading R-9): per level, u16
 // rank_block[b] = ones in [floor(b/128)*65536, b*512) and u64 rank_super[s] =
-// ones in [0, min(s*65536, n)).  The group passes accumulate raw per-block
-// counts (blkcnt); this file turns them into the two-level directory.
+// ones in [0, min(s*65536, n)).  k_rank_local popcounts the finished bitmaps
+// block by block; k_rank_super scans the superblock totals.
 #pragma once
 #include "wt_common.cuh"
 
@@ -13,9 +13,11 @@ namespace wtb {
 // A7 finalize: rank_block (u16, relative to the superblock) and rank_super.
 // k_rank_local: one warp per (level, superblock); k_rank_super: one CTA per level.
 // ---------------------------------------------------------------------------
-__global__ void k_rank_local(const uint32_t *__restrict__ blkcnt, uint64_t bpl, uint64_t nsup_data,
+__global__ void k_rank_local(const uint64_t *__restrict__ bits, uint64_t wpl, uint64_t bpl, uint64_t nsup_data,
                              uint32_t L, uint16_t *__restrict__ rank_block, uint64_t *__restrict__ suptot,
                              const uint32_t *err) {
+  // One warp per (level, superblock): popcount of its <= 128 blocks of 8 words
+  // (a streaming read of the finished bitmaps), then the in-superblock scan.
   if (*err) return;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -23,23 +25,28 @@ __global__ void k_rank_local(const uint32_t *__restrict__ blkcnt, uint64_t bpl, 
   const uint32_t l = (uint32_t)(gw / nsup_data);
   const uint64_t s = gw % nsup_data;
   const uint64_t b0 = s * 128;
+  const uint64_t *B = bits + (uint64_t)l * wpl;
   uint32_t v[4], sum = 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
-    uint64_t b = b0 + lane * 4 + i;
-    v[i] = b < bpl ? blkcnt[(uint64_t)l * bpl + b] : 0u;
-    sum += v[i];
-  }
-  uint32_t incl = sum;
+    const uint64_t b = b0 + lane * 4 + i;
+    uint32_t c = 0;
+    if (b < bpl) {
+      const ulonglong2 *w = reinterpret_cast<const ulonglong2 *>(B + b * 8);
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t t = __shfl_up_sync(FULL, incl, o);
-    if (lane >= o) incl += t;
+      for (int k = 0; k < 4; k++) {
+        const ulonglong2 x = __ldcs(w + k);
+        c += __popcll(x.x) + __popcll(x.y);
+      }
+    }
+    v[i] = c;
+    sum += c;
   }
+  const uint32_t incl = warp_incl_scan(sum, lane);
   uint32_t run = incl - sum;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
-    uint64_t b = b0 + lane * 4 + i;
+    const uint64_t b = b0 + lane * 4 + i;
     if (b < bpl) rank_block[(uint64_t)l * bpl + b] = (uint16_t)run;
     run += v[i];
   }

@@ -14,7 +14,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libwt_b200.so")
+# WT_LIB_PATH selects a tuning variant built by tools/tune.py (developer knob)
+_LIB_PATH = os.environ.get("WT_LIB_PATH") or os.path.join(_HERE, "libwt_b200.so")
 
 WT_OK, WT_EINVAL, WT_ESYMBOL, WT_ENOMEM, WT_ECUDA, WT_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 _NAMES = {WT_EINVAL: "WT_EINVAL", WT_ESYMBOL: "WT_ESYMBOL", WT_ENOMEM: "WT_ENOMEM",

@@ -1,0 +1,32 @@
+"""Build tuning variants of the library (-D defines) and time cfg builds with each.
+
+    python tools/tune.py build            # here (CPU): compile variants into tune_variants/
+    python tools/tune.py run 3 4          # on the GPU box: time configs with every variant
+"""
+import json, os, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VDIR = os.path.join(ROOT, "tune_variants")
+VARIANTS = {
+    "tw4k_w2": ["WT_TW=4096", "WT_GROUP_WARPS=2"],
+    "tw4k_w1": ["WT_TW=4096", "WT_GROUP_WARPS=1"],
+    "tw2k_w2": ["WT_TW=2048", "WT_GROUP_WARPS=2"],
+    "tw8k_w1": ["WT_TW=8192", "WT_GROUP_WARPS=1"],
+}
+CPW = os.environ.get("TUNE_CPW", "3").split(",")
+if sys.argv[1] == "build":
+    from paper_1407_8142_b200 import _build
+    os.makedirs(VDIR, exist_ok=True)
+    for name, defs in VARIANTS.items():
+        _build.build(force=True, defines=defs, out=os.path.join(VDIR, f"lib_{name}.so"))
+        print("built", name)
+else:
+    cfgs = sys.argv[2:] or ["4"]
+    for name in VARIANTS:
+      for cpw in CPW:
+        env = dict(os.environ, WT_LIB_PATH=os.path.join(VDIR, f"lib_{name}.so"), WT_CHAINS_PER_WARP=cpw)
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "probe.py"), *cfgs],
+                             capture_output=True, text=True, env=env, timeout=600)
+        lines = [l for l in out.stdout.splitlines() if l.startswith("cfg") or "k_group" in l]
+        print(f"== {name} cpw={cpw}")
+        print("\n".join(lines) if lines else out.stderr[-800:])
