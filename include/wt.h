@@ -50,7 +50,7 @@ extern "C" {
 #define WT_ESYMBOL (-2)     /* some S[i] >= sigma; no tree is produced              */
 #define WT_ENOMEM (-3)      /* device (or pinned host) allocation failed            */
 #define WT_ECUDA (-4)       /* a CUDA runtime call or kernel launch failed          */
-#define WT_EUNSUPPORTED (-5)/* valid input this build cannot handle yet (see below) */
+#define WT_EUNSUPPORTED (-5)/* reserved: valid input this build cannot handle        */
 
 /* Read-only view of a built tree.  Every array pointer is a DEVICE pointer
  * owned by the library; it stays valid until wt_free(). */
@@ -80,8 +80,8 @@ typedef struct wt_tree {
  *              retained after return.  Any alignment is accepted.
  *   n          sequence length, 0 <= n < 2^32.
  *   elem_bytes 1, 2 or 4.
- *   sigma      alphabet size, 1 <= sigma <= 2^(8*elem_bytes); this build
- *              supports L = ceil(log2 sigma) <= 16 (larger: WT_EUNSUPPORTED).
+ *   sigma      alphabet size, 1 <= sigma <= 2^(8*elem_bytes) (so up to 2^32,
+ *              L = ceil(log2 sigma) <= 32 levels).
  *   stream     cudaStream_t (as void*) on which all work is enqueued.
  *   out        receives the tree on success, NULL on any error.
  * Work is enqueued on `stream`, which is then synchronised ONCE to read the

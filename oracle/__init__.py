@@ -116,17 +116,23 @@ class OracleTree:
         self.supers_per_level = t.supers_per_level
         self.total_nodes = t.total_nodes
 
-    def arrays(self) -> dict:
+    def array(self, name: str) -> np.ndarray:
+        """Copy one output array out (keeps peak host memory low for big n)."""
         t = self._t.contents
         L = t.levels
-        return {
-            "bits": _copy(t.bits, L * t.words_per_level, np.uint64),
-            "level_node_ptr": _copy(t.level_node_ptr, L + 1, np.uint64),
-            "node_key": _copy(t.node_key, t.total_nodes, np.uint32),
-            "node_start": _copy(t.node_start, t.total_nodes, np.uint32),
-            "rank_block": _copy(t.rank_block, L * t.blocks_per_level, np.uint16),
-            "rank_super": _copy(t.rank_super, L * t.supers_per_level, np.uint64),
-        }
+        spec = {
+            "bits": (t.bits, L * t.words_per_level, np.uint64),
+            "level_node_ptr": (t.level_node_ptr, L + 1, np.uint64),
+            "node_key": (t.node_key, t.total_nodes, np.uint32),
+            "node_start": (t.node_start, t.total_nodes, np.uint32),
+            "rank_block": (t.rank_block, L * t.blocks_per_level, np.uint16),
+            "rank_super": (t.rank_super, L * t.supers_per_level, np.uint64),
+        }[name]
+        return _copy(*spec)
+
+    def arrays(self) -> dict:
+        return {k: self.array(k) for k in ("bits", "level_node_ptr", "node_key", "node_start",
+                                           "rank_block", "rank_super")}
 
     def access(self, positions) -> np.ndarray:
         return np.array([self._lib.oracle_access(self._t, int(i)) for i in positions],

@@ -48,7 +48,15 @@ struct GroupParams {
   uint32_t *chain_counter;
   uint64_t *bits;
   uint64_t wpl;
-  const uint32_t *err;
+  uint32_t *err;
+  // local mode (one tile per row; the row's own counts give its node starts)
+  uint32_t nk;                     // levels l0+1 .. l0+nk get their nodes emitted here
+  uint64_t rstride;
+  const uint32_t *rowoff;          // [k-1][row] exclusive prefix of node counts
+  const uint64_t *level_node_ptr;
+  const uint32_t *row_key;
+  uint32_t *node_key;
+  uint32_t *node_start;
 };
 
 constexpr uint32_t NO_CARRY = 0xffffffffu;
@@ -128,6 +136,7 @@ __device__ __forceinline__ void run_ends(WarpSmem<RecT> &ws, uint32_t slot, uint
 
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
 __global__ void __launch_bounds__(GROUP_WARPS * 32) k_group(GroupParams p) {
+  constexpr bool LOCAL = false;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpSmem<RecT> &ws = *reinterpret_cast<WarpSmem<RecT> *>(smem_raw + warp * sizeof(WarpSmem<RecT>));
@@ -147,12 +156,20 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32) k_group(GroupParams p) {
 
     // ---- chain geometry and its starting counts ----
     const uint32_t row = p.chain_row[c];
-    const uint32_t cfirst = p.row_first[row];
     const uint32_t cbeg = p.chain_begin[c], cend = p.chain_end[c];
     const uint32_t rstart = p.row_start[row];
-    const uint32_t *Crow = p.Cseg + (uint64_t)row * (ndig + 1);
-    for (uint32_t d = lane; d < ndig; d += 32)
-      ws.before[d] = p.E[(uint64_t)d * p.estride + c] - p.E[(uint64_t)d * p.estride + cfirst];
+    const uint32_t *Crow = LOCAL ? nullptr : p.Cseg + (uint64_t)row * (ndig + 1);
+    if (LOCAL && cend - cbeg > (uint32_t)TW) {  // not a one-tile row: the host falls back to chain mode
+      if (lane == 0) atomicOr(p.err, 2u);
+      continue;
+    }
+    if (LOCAL) {
+      for (uint32_t d = lane; d < ndig; d += 32) ws.before[d] = 0;
+    } else {
+      const uint32_t cfirst = p.row_first[row];
+      for (uint32_t d = lane; d < ndig; d += 32)
+        ws.before[d] = p.E[(uint64_t)d * p.estride + c] - p.E[(uint64_t)d * p.estride + cfirst];
+    }
     for (uint32_t i = lane; i < NDIG; i += 32) ws.CI[i] = NO_CARRY;
     __syncwarp();
 
@@ -240,8 +257,27 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32) k_group(GroupParams p) {
       }
 
       if constexpr (HAS_OUT) {  // key position = KB[digit] + final local position (A6)
-        for (uint32_t d = lane; d < ndig; d += 32) ws.KB[d] = rstart + Crow[d] + ws.before[d] - ws.Hl[d];
+        for (uint32_t d = lane; d < ndig; d += 32)
+          ws.KB[d] = LOCAL ? rstart : rstart + Crow[d] + ws.before[d] - ws.Hl[d];
         __syncwarp();
+      }
+      if constexpr (LOCAL) {  // A4: this row's nodes of levels l0+1 .. l0+nk (Fig. 1 l.18-20)
+        const uint32_t P = p.row_key[row];
+        for (uint32_t k = 1; k <= p.nk; k++) {
+          const uint32_t nq = 1u << k, sh = tau - k;
+          uint64_t j = p.level_node_ptr[p.l0 + k] + p.rowoff[(uint64_t)(k - 1) * p.rstride + row];
+          for (uint32_t q0 = 0; q0 < nq; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            const bool ne = q < nq && ws.Hl[(q + 1) << sh] > ws.Hl[q << sh];
+            const uint32_t bm = __ballot_sync(FULL, ne);
+            if (ne) {
+              const uint64_t jj = j + __popc(bm & lt);
+              p.node_key[jj] = (P << k) | q;
+              p.node_start[jj] = rstart + ws.Hl[q << sh];
+            }
+            j += __popc(bm);
+          }
+        }
       }
       OutT *ko = reinterpret_cast<OutT *>(p.keys_out);
 
@@ -267,7 +303,8 @@ __global__ void __launch_bounds__(GROUP_WARPS * 32) k_group(GroupParams p) {
             ws.T[2 * q] = (uint16_t)O;                    // O(gs)
             ws.T[2 * q + 1] = (uint16_t)(ge - (O + ones));  // ge - O(ge)
             O += ones;
-            ws.RG[q] = rstart + Crow[q << sh] + (ws.BX[(q + 1) << sh] - ws.BX[q << sh]);
+            ws.RG[q] = LOCAL ? rstart + ws.Hl[q << sh]
+                             : rstart + Crow[q << sh] + (ws.BX[(q + 1) << sh] - ws.BX[q << sh]);
           }
         }
         __syncwarp();

@@ -6,6 +6,7 @@
 // and the node counts.
 #include "wt.h"
 #include "wt_group.cuh"
+#include "wt_local.cuh"
 #include "wt_prep.cuh"
 #include "wt_rank.cuh"
 
@@ -173,26 +174,85 @@ GroupLaunch group_launch() {
   return gl;
 }
 
-GroupLaunch pick_group(uint32_t g, uint32_t NG, uint32_t eb) {
-  const bool has_out = g + 1 < NG;
-  if (g > 0) return group_launch<uint8_t, uint8_t, uint8_t, false>();
-  if (!has_out) {
-    if (eb == 1) return group_launch<uint8_t, uint8_t, uint8_t, false>();
-    if (eb == 2) return group_launch<uint16_t, uint8_t, uint8_t, false>();
-    return group_launch<uint32_t, uint8_t, uint8_t, false>();
-  }
-  if (eb == 2) return group_launch<uint16_t, uint16_t, uint8_t, true>();
-  return group_launch<uint32_t, uint16_t, uint8_t, true>();
+struct LocalLaunch {
+  void (*count)(LocalParams) = nullptr;
+  void (*build)(LocalParams) = nullptr;
+  size_t smem = 0;
+  int grid = 0;
+};
+
+template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
+LocalLaunch local_launch() {
+  static LocalLaunch ll;
+  static std::once_flag f;
+  std::call_once(f, [] {
+    ll.count = k_local<InT, RecT, OutT, HAS_OUT, true>;
+    ll.build = k_local<InT, RecT, OutT, HAS_OUT, false>;
+    ll.smem = LOCAL_WARPS * sizeof(LocalSmem<RecT>);
+    cudaFuncSetAttribute(ll.count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem);
+    cudaFuncSetAttribute(ll.build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ll.build, LOCAL_WARPS * 32, ll.smem);
+    ll.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
+  });
+  return ll;
 }
 
-// Per-group scratch: chains, rows, digit tables.
+LocalLaunch pick_local(uint32_t inw, uint32_t recw, uint32_t outw, bool has_out) {
+  if (!has_out) {
+    if (recw == 1) {
+      if (inw == 1) return local_launch<uint8_t, uint8_t, uint8_t, false>();
+      if (inw == 2) return local_launch<uint16_t, uint8_t, uint8_t, false>();
+      return local_launch<uint32_t, uint8_t, uint8_t, false>();
+    }
+    return LocalLaunch{};
+  }
+  if (recw == 2) {
+    if (inw == 2) return local_launch<uint16_t, uint16_t, uint8_t, true>();
+    return local_launch<uint32_t, uint16_t, uint8_t, true>();
+  }
+  if (outw == 2) return local_launch<uint32_t, uint32_t, uint16_t, true>();
+  return local_launch<uint32_t, uint32_t, uint32_t, true>();
+}
+
+// bytes of an unsigned integer holding `bits` bits
+uint32_t width_of(uint32_t bits) { return bits <= 8 ? 1u : (bits <= 16 ? 2u : 4u); }
+
+// k_group instantiation for (input width, record width, output width, local?)
+GroupLaunch pick_group_mode(uint32_t inw, uint32_t recw, uint32_t outw, bool has_out) {
+  if (!has_out) {
+    if (recw == 1) {
+      if (inw == 1) return group_launch<uint8_t, uint8_t, uint8_t, false>();
+      if (inw == 2) return group_launch<uint16_t, uint8_t, uint8_t, false>();
+      return group_launch<uint32_t, uint8_t, uint8_t, false>();
+    }
+    return GroupLaunch{};  // the last group always has <= 8 bits per record
+  }
+  if (recw == 2) {
+    if (inw == 2) return group_launch<uint16_t, uint16_t, uint8_t, true>();
+    return group_launch<uint32_t, uint16_t, uint8_t, true>();
+  }
+  // recw == 4
+  if (outw == 2) return group_launch<uint32_t, uint32_t, uint16_t, true>();
+  return group_launch<uint32_t, uint32_t, uint32_t, true>();
+}
+
+// Per-group scratch: chains, rows, digit tables, node-count scans.
 struct GroupBufs {
-  uint32_t tau = 0, l0 = 0, pbits = 0, ndig = 0;
+  uint32_t tau = 0, l0 = 0, pbits = 0, ndig = 0, nk = 0, k_lo = 0;
+  uint32_t inw = 0, recw = 0, outw = 0;
+  bool local = false;
   uint64_t CH = TW, max_chains = 0, max_rows = 0;
   GroupLaunch gl;
+  LocalLaunch ll;
+  uint32_t nbatch = 0;
+  uint32_t *batch_first = nullptr, *bcounts = nullptr;
+  void *keys_out = nullptr;
   uint32_t *chain_begin = nullptr, *chain_end = nullptr, *chain_row = nullptr;
   uint32_t *row_first = nullptr, *row_start = nullptr, *row_key = nullptr;
   uint32_t *E = nullptr, *Cseg = nullptr;
+  uint32_t *rowcnt = nullptr, *bsum = nullptr;
+  uint32_t nblk = 0;
   uint32_t *counts = nullptr;  // [0] chains, [1] rows, [2] chain claim counter
   void alloc(Allocs &A) {
     chain_begin = A.alloc<uint32_t>(max_chains, false);
@@ -201,14 +261,26 @@ struct GroupBufs {
     row_first = A.alloc<uint32_t>(max_rows + 1, false);
     row_start = A.alloc<uint32_t>(max_rows, false);
     row_key = A.alloc<uint32_t>(max_rows, false);
-    E = A.alloc<uint32_t>((uint64_t)ndig * (max_chains + 1), false);
-    Cseg = A.alloc<uint32_t>(max_rows * (ndig + 1), false);
+    if (!local) {
+      E = A.alloc<uint32_t>((uint64_t)ndig * (max_chains + 1), false);
+      Cseg = A.alloc<uint32_t>(max_rows * (ndig + 1), false);
+    }
+    const uint64_t nunits = local ? nbatch : max_rows;  // node counts per batch (local) or row
+    nblk = (uint32_t)((nunits + SCAN_BLK - 1) / SCAN_BLK);
+    if (nk) {
+      rowcnt = A.alloc<uint32_t>((uint64_t)nk * nunits, false);
+      bsum = A.alloc<uint32_t>((uint64_t)nk * nblk, false);
+    }
+    if (local) {
+      batch_first = A.alloc<uint32_t>(nbatch + 1, false);
+      bcounts = A.alloc<uint32_t>(4, false);
+    }
     counts = A.alloc<uint32_t>(4, false);
   }
 };
 
 int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n, uint32_t eb,
-               uint64_t sigma, void *stream_v, wt_tree **out) {
+               uint64_t sigma, void *stream_v, wt_tree **out, bool force_chain) {
   if (!out) return WT_EINVAL;
   *out = nullptr;
   if (eb != 1 && eb != 2 && eb != 4) return WT_EINVAL;
@@ -216,7 +288,6 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   if (n >= (1ull << 32)) return WT_EINVAL;
   if (n > 0 && !(from_host ? h_seq : d_seq)) return WT_EINVAL;
   const uint32_t L = levels_of(sigma);
-  if (L > 16) return WT_EUNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream_v);
   configure_pool_once();
 
@@ -260,33 +331,52 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     seq = d;
   }
 
-  // ---- plan: groups of <= 8 levels, chains sized to ~3 per resident warp ----
+  // ---- plan: groups of <= 8 levels ----
   const uint32_t NG = (L + TAU_MAX - 1) / TAU_MAX;
-  GroupBufs G[2];
+  GroupBufs G[4];
   for (uint32_t g = 0; g < NG; g++) {
     GroupBufs &gb = G[g];
     gb.l0 = g * TAU_MAX;
     gb.tau = std::min<uint32_t>(TAU_MAX, L - gb.l0);
     gb.pbits = L - gb.l0 - gb.tau;
     gb.ndig = 1u << gb.tau;
-    gb.gl = pick_group(g, NG, eb);
-    const uint64_t warps = (uint64_t)gb.gl.grid * GROUP_WARPS;
-    static const uint64_t cpw = getenv("WT_CHAINS_PER_WARP") ? strtoull(getenv("WT_CHAINS_PER_WARP"), 0, 10) : 8;
-    const uint64_t target = (n + cpw * warps - 1) / (cpw * warps);
-    gb.CH = std::max<uint64_t>(TW, ((target + TW - 1) / TW) * TW);
-    if (g == 0) {
-      gb.max_chains = std::max<uint64_t>((n + gb.CH - 1) / gb.CH, 1);
-      gb.max_rows = 1;
+    gb.k_lo = g == 0 ? 0u : 1u;
+    gb.inw = g == 0 ? eb : width_of(L - gb.l0);
+    gb.recw = width_of(L - gb.l0);
+    gb.outw = width_of(gb.pbits);
+    const bool has_out = g + 1 < NG;
+    gb.max_rows = g == 0 ? 1 : std::min<uint64_t>(1ull << gb.l0, std::max<uint64_t>(n, 1));
+    // local mode when level-l0 nodes are small on average (one tile per row)
+    gb.local = !force_chain && g > 0 && n / gb.max_rows <= (uint64_t)TW / 8;
+    const uint32_t k_hi = std::min<uint32_t>(gb.tau, L - 1 - gb.l0);
+    gb.nk = k_hi >= gb.k_lo ? k_hi - gb.k_lo + 1 : 0;
+    if (gb.local) gb.ll = pick_local(gb.inw, gb.recw, gb.outw, has_out);
+    else gb.gl = pick_group_mode(gb.inw, gb.recw, gb.outw, has_out);
+    if (gb.local ? !gb.ll.build : !gb.gl.kern) {
+      A.free_scratch();
+      A.free_outputs();
+      cudaStreamSynchronize(s);
+      delete t;
+      return WT_EUNSUPPORTED;
+    }
+    if (gb.local) {
+      gb.nbatch = (uint32_t)((n + TW - 1) / TW);
+      gb.max_chains = 1;
     } else {
-      gb.max_rows = std::min<uint64_t>(1ull << gb.l0, std::max<uint64_t>(n, 1));
-      gb.max_chains = (n + gb.CH - 1) / gb.CH + gb.max_rows;
+      const uint64_t warps = (uint64_t)gb.gl.grid * GROUP_WARPS;
+      static const uint64_t cpw =
+          getenv("WT_CHAINS_PER_WARP") ? strtoull(getenv("WT_CHAINS_PER_WARP"), 0, 10) : 8;
+      const uint64_t target = (n + cpw * warps - 1) / (cpw * warps);
+      gb.CH = std::max<uint64_t>(TW, ((target + TW - 1) / TW) * TW);
+      gb.max_chains = g == 0 ? std::max<uint64_t>((n + gb.CH - 1) / gb.CH, 1)
+                             : (n + gb.CH - 1) / gb.CH + gb.max_rows;
     }
     gb.alloc(A);
+    if (has_out) gb.keys_out = A.alloc<uint8_t>(n * gb.outw, false);
   }
   uint32_t *err = A.alloc<uint32_t>(4, false);
   uint32_t *ncount = A.alloc<uint32_t>(L + 1, false);
   uint64_t *suptot = A.alloc<uint64_t>(L * NSD, false);
-  void *keys1 = NG > 1 ? (void *)A.alloc<uint8_t>(n, false) : nullptr;
 
   static uint64_t *h_stage = nullptr;  // pinned staging for the single D2H
   static std::mutex stage_mu;
@@ -313,6 +403,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   if (L && n) chk(cudaMemsetAsync(t->bits, 0, L * WPL * sizeof(uint64_t), s));
   for (uint32_t g = 0; g < NG; g++) chk(cudaMemsetAsync(G[g].counts, 0, 4 * sizeof(uint32_t), s));
 
+  const void *keys_in = seq;
   for (uint32_t g = 0; g < NG || (g == 0 && L == 0); g++) {
     // ---- chains of this group + their digit histograms (A1 for g = 0) ----
     if (g == 0) {
@@ -337,16 +428,72 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
         chk(cudaGetLastError());
         rec.begin("k_hist", n * eb);
         const uint32_t shift = L - tau0;
+        const unsigned grid = std::min<uint32_t>(K, 4 * num_sms());
         if (eb == 1)
-          k_chain_hist<uint8_t, true><<<std::min<uint32_t>(K, 4 * num_sms()), 512, 0, s>>>((const uint8_t *)seq, sigma, shift, ndig0, cb, ce_, cnt, stride, E, err);
+          k_chain_hist<uint8_t, true><<<grid, 512, 0, s>>>((const uint8_t *)seq, sigma, shift, ndig0, cb, ce_, cnt, stride, E, err);
         else if (eb == 2)
-          k_chain_hist<uint16_t, true><<<std::min<uint32_t>(K, 4 * num_sms()), 512, 0, s>>>((const uint16_t *)seq, sigma, shift, ndig0, cb, ce_, cnt, stride, E, err);
+          k_chain_hist<uint16_t, true><<<grid, 512, 0, s>>>((const uint16_t *)seq, sigma, shift, ndig0, cb, ce_, cnt, stride, E, err);
         else
-          k_chain_hist<uint32_t, true><<<std::min<uint32_t>(K, 4 * num_sms()), 512, 0, s>>>((const uint32_t *)seq, sigma, shift, ndig0, cb, ce_, cnt, stride, E, err);
+          k_chain_hist<uint32_t, true><<<grid, 512, 0, s>>>((const uint32_t *)seq, sigma, shift, ndig0, cb, ce_, cnt, stride, E, err);
         chk(cudaGetLastError());
         rec.end();
       }
       if (!NG || !n) break;
+    } else if (G[g].local) {
+      // ======== local mode: batches of small level-l0 nodes, finished per warp ========
+      GroupBufs &gb = G[g];
+      rec.begin("k_rows", gb.max_rows * 8);
+      k_rows_from_nodes<<<(unsigned)std::min<uint64_t>((gb.max_rows + 255) / 256, 65535), 256, 0, s>>>(
+          t->level_node_ptr, ncount, gb.l0, t->node_key, t->node_start, gb.row_start, gb.row_key, gb.counts, err);
+      k_batches<<<(gb.nbatch + 256) / 256, 256, 0, s>>>(gb.row_start, gb.counts, gb.nbatch, gb.batch_first,
+                                                         gb.bcounts, err);
+      chk(cudaGetLastError());
+      chk(cudaMemsetAsync(gb.bcounts, 0, sizeof(uint32_t), s));  // [0] = batch claim counter
+      rec.end();
+      LocalParams lp{};
+      lp.keys_in = keys_in;
+      lp.keys_out = gb.keys_out;
+      lp.n = n;
+      lp.l0 = gb.l0;
+      lp.tau = gb.tau;
+      lp.pbits = gb.pbits;
+      lp.nk = gb.nk;
+      lp.nbatch = gb.nbatch;
+      lp.batch_first = gb.batch_first;
+      lp.counts = gb.counts;
+      lp.row_start = gb.row_start;
+      lp.row_key = gb.row_key;
+      lp.batch_counter = gb.bcounts;
+      lp.batchcnt = gb.rowcnt;
+      lp.level_node_ptr = t->level_node_ptr;
+      lp.node_key = t->node_key;
+      lp.node_start = t->node_start;
+      lp.bits = t->bits;
+      lp.wpl = WPL;
+      lp.err = err;
+      if (gb.nk) {
+        // A4 pass 1: node counts per batch and level, then their scan (CSR offsets)
+        rec.begin("k_local_count", n * gb.inw);
+        gb.ll.count<<<gb.ll.grid, LOCAL_WARPS * 32, gb.ll.smem, s>>>(lp);
+        chk(cudaGetLastError());
+        k_scan_rows_1<<<dim3(gb.nblk, gb.nk), 1024, 0, s>>>(gb.rowcnt, gb.nbatch, gb.bcounts, gb.bsum, gb.nblk, err);
+        k_scan_rows_2<<<gb.nk, 1024, 0, s>>>(gb.bsum, gb.nblk, gb.bcounts, gb.l0, gb.k_lo, gb.nk, L, ncount,
+                                             t->level_node_ptr, err);
+        k_scan_rows_3<<<dim3(gb.nblk, gb.nk), 1024, 0, s>>>(gb.rowcnt, gb.nbatch, gb.bcounts, gb.bsum, gb.nblk, err);
+        k_level_ptr<<<1, 32, 0, s>>>(ncount, gb.l0, gb.k_lo, gb.nk, L, t->level_node_ptr, err);
+        chk(cudaMemsetAsync(gb.bcounts, 0, sizeof(uint32_t), s));
+        chk(cudaGetLastError());
+        rec.end();
+      }
+      const bool has_out = g + 1 < NG;
+      char name[32];
+      snprintf(name, sizeof(name), "k_group%u", g);
+      rec.begin(name, n * gb.inw + (has_out ? n * gb.outw : 0) + (uint64_t)gb.tau * n / 8);
+      gb.ll.build<<<gb.ll.grid, LOCAL_WARPS * 32, gb.ll.smem, s>>>(lp);
+      chk(cudaGetLastError());
+      rec.end();
+      keys_in = gb.keys_out;
+      continue;
     } else {
       GroupBufs &gb = G[g];
       rec.begin("k_chains", gb.max_chains * 12);
@@ -355,13 +502,22 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
                                              gb.row_start, gb.row_key, gb.counts, err);
       chk(cudaGetLastError());
       rec.end();
-      rec.begin("k_seg_hist", n);
-      k_chain_hist<uint8_t, false><<<(unsigned)std::min<uint64_t>(gb.max_chains, 4 * num_sms()), 512, 0, s>>>(
-          (const uint8_t *)keys1, sigma, gb.pbits, gb.ndig, gb.chain_begin, gb.chain_end, gb.counts,
-          (uint32_t)gb.max_chains + 1, gb.E, err);
+      rec.begin("k_seg_hist", n * gb.inw);
+      const unsigned grid = (unsigned)std::min<uint64_t>(gb.max_chains, 4 * num_sms());
+      const uint32_t estr = (uint32_t)gb.max_chains + 1;
+      if (gb.inw == 1)
+        k_chain_hist<uint8_t, false><<<grid, 512, 0, s>>>((const uint8_t *)keys_in, sigma, gb.pbits, gb.ndig,
+                                                          gb.chain_begin, gb.chain_end, gb.counts, estr, gb.E, err);
+      else if (gb.inw == 2)
+        k_chain_hist<uint16_t, false><<<grid, 512, 0, s>>>((const uint16_t *)keys_in, sigma, gb.pbits, gb.ndig,
+                                                           gb.chain_begin, gb.chain_end, gb.counts, estr, gb.E, err);
+      else
+        k_chain_hist<uint32_t, false><<<grid, 512, 0, s>>>((const uint32_t *)keys_in, sigma, gb.pbits, gb.ndig,
+                                                           gb.chain_begin, gb.chain_end, gb.counts, estr, gb.E, err);
       chk(cudaGetLastError());
       rec.end();
     }
+    // ======== chain mode ========
     GroupBufs &gb = G[g];
     const uint32_t stride = (uint32_t)gb.max_chains + 1;
     rec.begin("k_chain_scan", (uint64_t)gb.ndig * gb.max_chains * 8);
@@ -373,27 +529,31 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
                                                                           gb.ndig, gb.Cseg, err);
     chk(cudaGetLastError());
     rec.end();
-    // ---- A4: node table of this group's levels ----
-    {
-      const uint32_t k_lo = g == 0 ? 0u : 1u;
-      const uint32_t k_hi = std::min<uint32_t>(gb.tau, L - 1 - gb.l0);  // inclusive
-      if (k_hi >= k_lo) {
-        rec.begin("k_nodes_count", 0);
-        k_nodes_count<<<k_hi - k_lo + 1, 1024, 0, s>>>(gb.Cseg, gb.counts, gb.tau, gb.l0, k_lo, ncount, err);
-        chk(cudaGetLastError());
-        rec.end();
-        rec.begin("k_nodes_emit", 0);
-        k_nodes_emit<<<k_hi - k_lo + 1, 1024, 0, s>>>(gb.Cseg, gb.counts, gb.tau, gb.l0, k_lo, L, gb.row_key,
-                                                      gb.row_start, ncount, t->level_node_ptr, t->node_key,
-                                                      t->node_start, err);
-        chk(cudaGetLastError());
-        rec.end();
-      }
+    // ---- A4: node table of this group's levels l0+k_lo .. l0+k_lo+nk-1 ----
+    if (gb.nk) {
+      const uint64_t rstride = gb.max_rows;
+      const unsigned cgrid = (unsigned)std::min<uint64_t>((gb.max_rows * gb.nk + 255) / 256, 65535);
+      rec.begin("k_nodes_count", 0);
+      k_row_nodes_count<<<cgrid, 256, 0, s>>>(gb.Cseg, gb.counts, gb.tau, gb.k_lo, gb.nk, rstride, gb.rowcnt, err);
+      chk(cudaGetLastError());
+      k_scan_rows_1<<<dim3(gb.nblk, gb.nk), 1024, 0, s>>>(gb.rowcnt, rstride, gb.counts, gb.bsum, gb.nblk, err);
+      k_scan_rows_2<<<gb.nk, 1024, 0, s>>>(gb.bsum, gb.nblk, gb.counts, gb.l0, gb.k_lo, gb.nk, L, ncount,
+                                           t->level_node_ptr, err);
+      k_scan_rows_3<<<dim3(gb.nblk, gb.nk), 1024, 0, s>>>(gb.rowcnt, rstride, gb.counts, gb.bsum, gb.nblk, err);
+      k_level_ptr<<<1, 32, 0, s>>>(ncount, gb.l0, gb.k_lo, gb.nk, L, t->level_node_ptr, err);
+      chk(cudaGetLastError());
+      rec.end();
+      rec.begin("k_nodes_emit", 0);
+      k_row_nodes_emit<<<cgrid, 256, 0, s>>>(gb.Cseg, gb.counts, gb.tau, gb.l0, gb.k_lo, gb.nk, rstride, gb.rowcnt,
+                                             t->level_node_ptr, gb.row_key, gb.row_start, t->node_key,
+                                             t->node_start, err);
+      chk(cudaGetLastError());
+      rec.end();
     }
     // ---- the fused tau-level pass ----
     GroupParams gp{};
-    gp.keys_in = g == 0 ? seq : keys1;
-    gp.keys_out = (g + 1 < NG) ? keys1 : nullptr;
+    gp.keys_in = keys_in;
+    gp.keys_out = gb.keys_out;
     gp.n = n;
     gp.l0 = gb.l0;
     gp.tau = gb.tau;
@@ -412,13 +572,13 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     gp.wpl = WPL;
     gp.err = err;
     const bool has_out = g + 1 < NG;
-    const uint64_t in_bytes = g == 0 ? n * eb : n;
     char name[32];
     snprintf(name, sizeof(name), "k_group%u", g);
-    rec.begin(name, in_bytes + (has_out ? n : 0) + (uint64_t)gb.tau * n / 8);
+    rec.begin(name, n * gb.inw + (has_out ? n * gb.outw : 0) + (uint64_t)gb.tau * n / 8);
     gb.gl.kern<<<gb.gl.grid, GROUP_WARPS * 32, gb.gl.smem, s>>>(gp);
     chk(cudaGetLastError());
     rec.end();
+    keys_in = gb.keys_out;
   }
 
   if (L > 0 && n > 0) {
@@ -459,7 +619,9 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     A.free_outputs();
     cudaStreamSynchronize(s);
     delete t;
-    return WT_ESYMBOL;
+    if (errflag & 1u) return WT_ESYMBOL;
+    // a level-l0 node too large for local mode: rebuild with chain mode everywhere
+    return force_chain ? WT_ECUDA : build_impl(d_seq, h_seq, from_host, n, eb, sigma, stream_v, out, true);
   }
   Internal *in = new Internal();
   in->stream = s;
@@ -474,12 +636,12 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
 extern "C" {
 
 int wt_build(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma, void *stream, wt_tree **out) {
-  return build_impl(d_seq, nullptr, false, n, elem_bytes, sigma, stream, out);
+  return build_impl(d_seq, nullptr, false, n, elem_bytes, sigma, stream, out, false);
 }
 
 int wt_build_host(const void *h_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma, void *stream,
                   wt_tree **out) {
-  return build_impl(nullptr, h_seq, true, n, elem_bytes, sigma, stream, out);
+  return build_impl(nullptr, h_seq, true, n, elem_bytes, sigma, stream, out, false);
 }
 
 int wt_free(wt_tree *t) {

@@ -1,0 +1,313 @@
+// wt_local.cuh -- the deep-level pass for groups whose level-l0 nodes are small
+// (local mode; config 5 levels 24..31: ~16.7M nodes of ~32 symbols).
+//
+// The subtree of a level-l0 node ("row") occupies the same contiguous range
+// [row_start, row_end) at every deeper level (a node's
+// children partition its symbols), so a row can be finished entirely inside
+// one warp, with no global counts: the row's own digit histogram gives every
+// node start below it.  A warp takes a BATCH of consecutive rows (those whose
+// start lies in one TW-sized window of positions); the batch covers a
+// contiguous range [A, B) at each of the tau levels, so its bits are staged in
+// shared memory and written with only the two edge words shared (A5).
+//
+// Per row:
+//  * <= 32 symbols: register path, one symbol per lane, no data movement: the
+//    position of a symbol at local level k is
+//        pos_k = #{row symbols whose k-bit prefix is smaller}
+//              + #{earlier row symbols with the same k-bit prefix}
+//    (the stable order of Fig. 1 / PAPER.md:468-475), maintained with two lane
+//    masks (lt: smaller prefix, eq: same prefix) updated by one ballot per
+//    level; the level's bits are one warp OR-reduction of (bit << pos_k).
+//  * larger rows: the tile path of k_group (shared-memory stable splits with
+//    the row's split tables), bits copied into the batch staging.
+// Node tables (A4): pass 1 (COUNT) counts each batch's nodes per level; after
+// a scan over batches, pass 2 writes them in (level, row, prefix) order.
+#pragma once
+#include "wt_common.cuh"
+
+namespace wtb {
+
+struct LocalParams {
+  const void *keys_in;
+  void *keys_out;
+  uint64_t n;
+  uint32_t l0, tau, pbits, nk;  // nodes of levels l0+1 .. l0+nk are emitted here
+  uint32_t nbatch;
+  const uint32_t *batch_first;  // first row of each batch, [nbatch + 1]
+  const uint32_t *counts;       // [1] = rows
+  const uint32_t *row_start;    // start of each row (level-l0 node)
+  const uint32_t *row_key;      // its key (top-l0-bit prefix)
+  uint32_t *batch_counter;
+  uint32_t *batchcnt;           // [k-1][nbatch]: pass 1 counts, then exclusive offsets
+  const uint64_t *level_node_ptr;
+  uint32_t *node_key;
+  uint32_t *node_start;
+  uint64_t *bits;
+  uint64_t wpl;
+  uint32_t *err;
+};
+
+template <typename RecT>
+struct LocalSmem {
+  alignas(16) RecT buf[2][TW];
+  alignas(16) uint32_t SB[TAU_MAX][2 * NCH + 2];  // batch staging bitmaps (<= 2*TW bits)
+  alignas(16) uint32_t LB[NCH];
+  uint32_t hist2[NDIG / 2];
+  uint16_t Hl[NDIG + 2];
+  uint16_t T[NDIG];
+};
+
+constexpr int LOCAL_WARPS = 2;
+
+// OR `nbits` (<= 32) bits of v into the staging bitmap at bit offset `off`.
+__device__ __forceinline__ void stage_bits(uint32_t *SB, uint32_t off, uint32_t v) {
+  const uint32_t w = off >> 5, sh = off & 31;
+  SB[w] |= v << sh;
+  if (sh) SB[w + 1] |= v >> (32 - sh);
+}
+
+template <typename InT, typename RecT, typename OutT, bool HAS_OUT, bool COUNT>
+__global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  LocalSmem<RecT> &ws = *reinterpret_cast<LocalSmem<RecT> *>(smem_raw + warp * sizeof(LocalSmem<RecT>));
+  if (ld_relaxed(p.err)) return;
+  const InT *keys = reinterpret_cast<const InT *>(p.keys_in);
+  OutT *ko = reinterpret_cast<OutT *>(p.keys_out);
+  const uint32_t tau = p.tau, pbits = p.pbits, ndig = 1u << tau;
+  const uint32_t pmask = (1u << pbits) - 1u;
+  const uint32_t nrows = p.counts[1];
+  const uint32_t lt = lanemask_lt();
+
+  while (true) {
+    uint32_t b = 0;
+    if (lane == 0) b = atomicAdd(p.batch_counter, 1u);
+    b = __shfl_sync(FULL, b, 0);
+    if (b >= p.nbatch) break;
+    const uint32_t r0 = p.batch_first[b], r1 = p.batch_first[b + 1];
+    if (r0 >= r1) {  // no row starts in this window: it contributes no nodes
+      if (COUNT && lane < (int)p.nk) p.batchcnt[(uint64_t)lane * p.nbatch + b] = 0;
+      continue;
+    }
+    const uint32_t A = p.row_start[r0];
+    const uint32_t Bend = r1 < nrows ? p.row_start[r1] : (uint32_t)p.n;
+    if (Bend - A > 2u * TW) {  // a row larger than TW: the host falls back to chain mode
+      if (lane == 0) atomicOr(p.err, 2u);
+      continue;
+    }
+    const uint32_t nsw = ((Bend - A) + 31) / 32 + 1;  // staging words used
+    if (!COUNT) {
+      for (uint32_t k = 0; k < tau; k++)
+        for (uint32_t w = lane; w < nsw; w += 32) ws.SB[k][w] = 0;
+    }
+    // running node offsets (lane kk holds level l0+1+kk), from the batch scan
+    uint32_t nodeoff = 0;
+    if (lane < (int)p.nk) nodeoff = COUNT ? 0u : p.batchcnt[(uint64_t)lane * p.nbatch + b];
+    __syncwarp();
+
+    for (uint32_t r = r0; r < r1; r++) {
+      const uint32_t rs = p.row_start[r];
+      const uint32_t re = r + 1 < nrows ? p.row_start[r + 1] : (uint32_t)p.n;
+      const uint32_t len = re - rs;
+      const uint32_t P = p.row_key[r];
+      const uint32_t soff = rs - A;  // the row's bit offset inside the batch staging
+      if (len <= 32) {
+        // ---------------- register path ----------------
+        const bool valid = (uint32_t)lane < len;
+        const uint32_t key = valid ? (uint32_t)keys[rs + lane] : 0u;
+        const uint32_t dig = (key >> pbits) & (ndig - 1u);
+        uint32_t eq = __ballot_sync(FULL, valid), ltm = 0;  // same prefix / smaller prefix (this row)
+        for (uint32_t k = 0; k < tau; k++) {
+          const uint32_t bit = (dig >> (tau - 1u - k)) & 1u;
+          const uint32_t m = __ballot_sync(FULL, valid && bit);
+          if (!COUNT) {
+            const uint32_t pos = __popc(ltm) + __popc(eq & lt);  // position at level l0+k
+            const uint32_t word = __reduce_or_sync(FULL, valid && bit ? (1u << pos) : 0u);
+            if (lane == 0) stage_bits(ws.SB[k], soff, word);
+          }
+          // refine to the (k+1)-bit prefix: same group and same bit; smaller if bit 0 vs my 1
+          if (bit) {
+            ltm |= eq & ~m;
+            eq &= m;
+          } else {
+            eq &= ~m;
+          }
+          if (k + 1 <= p.nk) {  // nodes of level l0+k+1 = distinct (k+1)-bit prefixes
+            const bool first = valid && (eq & lt) == 0;
+            const uint32_t fm = __ballot_sync(FULL, first);
+            const uint32_t base = __shfl_sync(FULL, nodeoff, k);  // lane k holds level l0+k+1
+            if (!COUNT && first) {
+              const uint64_t j = p.level_node_ptr[p.l0 + k + 1] + base + __popc(fm & ltm);  // leaders with a smaller prefix
+              p.node_key[j] = (P << (k + 1)) | (dig >> (tau - 1u - k));
+              p.node_start[j] = rs + __popc(ltm);
+            }
+            if (lane == (int)k) nodeoff += __popc(fm);
+          }
+        }
+        if (HAS_OUT && !COUNT && valid) ko[rs + __popc(ltm) + __popc(eq & lt)] = (OutT)(key & pmask);
+        continue;
+      }
+      // ---------------- tile path (32 < len <= TW) ----------------
+      if (len > (uint32_t)TW) {
+        if (lane == 0) atomicOr(p.err, 2u);
+        break;
+      }
+      const uint32_t nch = (len + 31) >> 5;
+      for (uint32_t d = lane; d < NDIG / 2; d += 32) ws.hist2[d] = 0;
+      __syncwarp();
+      for (uint32_t pos = lane; pos < len; pos += 32) {
+        const uint32_t key = (uint32_t)keys[rs + pos];
+        const uint32_t dig = (key >> pbits) & (ndig - 1u);
+        ws.buf[0][pos] = (RecT)((dig << pbits) | (key & pmask));
+        atomicAdd(&ws.hist2[dig >> 1], 1u << ((dig & 1u) << 4));
+      }
+      __syncwarp();
+      {  // Hl = exclusive scan of the row's digit counts
+        const uint32_t per = (ndig + 31) >> 5;
+        const uint32_t lo = min(lane * per, ndig), hi = min(lo + per, ndig);
+        uint32_t s1 = 0;
+        for (uint32_t d = lo; d < hi; d++) s1 += (ws.hist2[d >> 1] >> ((d & 1u) << 4)) & 0xffffu;
+        const uint32_t i1 = warp_incl_scan(s1, lane);
+        uint32_t r1v = i1 - s1;
+        for (uint32_t d = lo; d < hi; d++) {
+          ws.Hl[d] = (uint16_t)r1v;
+          r1v += (ws.hist2[d >> 1] >> ((d & 1u) << 4)) & 0xffffu;
+        }
+        if (lane == 31) ws.Hl[ndig] = (uint16_t)i1;
+        __syncwarp();
+      }
+      // nodes of levels l0+1 .. l0+nk (Fig. 1 l.18-20)
+      for (uint32_t k = 1; k <= p.nk; k++) {
+        const uint32_t nq = 1u << k, sh = tau - k;
+        uint32_t base = __shfl_sync(FULL, nodeoff, k - 1);
+        for (uint32_t q0 = 0; q0 < nq; q0 += 32) {
+          const uint32_t q = q0 + lane;
+          const bool ne = q < nq && ws.Hl[(q + 1) << sh] > ws.Hl[q << sh];
+          const uint32_t bm = __ballot_sync(FULL, ne);
+          if (!COUNT && ne) {
+            const uint64_t j = p.level_node_ptr[p.l0 + k] + base + __popc(bm & lt);
+            p.node_key[j] = (P << k) | q;
+            p.node_start[j] = rs + ws.Hl[q << sh];
+          }
+          base += __popc(bm);
+        }
+        if (lane == (int)(k - 1)) nodeoff = base;
+      }
+      if constexpr (!COUNT) {
+      for (uint32_t k = 0; k < tau; k++) {
+        const uint32_t nq = 1u << k, sh = tau - k;
+        const bool do_split = HAS_OUT || (k + 1 < tau);
+        const uint32_t bitmask = 1u << (pbits + tau - 1u - k);
+        const uint32_t bitsh = pbits + tau - 1u - k;
+        const RecT *src = ws.buf[k & 1];
+        RecT *dst = ws.buf[(k + 1) & 1];
+        {  // split table T_k of the row
+          const uint32_t per = (nq + 31) >> 5;
+          const uint32_t lo = min(lane * per, nq), hi = min(lo + per, nq);
+          uint32_t sacc = 0;
+          for (uint32_t q = lo; q < hi; q++) sacc += ws.Hl[(2 * q + 2) << (sh - 1)] - ws.Hl[(2 * q + 1) << (sh - 1)];
+          const uint32_t incl = warp_incl_scan(sacc, lane);
+          uint32_t O = incl - sacc;
+          for (uint32_t q = lo; q < hi; q++) {
+            const uint32_t ge = ws.Hl[(q + 1) << sh];
+            const uint32_t ones = ws.Hl[(2 * q + 2) << (sh - 1)] - ws.Hl[(2 * q + 1) << (sh - 1)];
+            ws.T[2 * q] = (uint16_t)O;
+            ws.T[2 * q + 1] = (uint16_t)(ge - (O + ones));
+            O += ones;
+          }
+        }
+        __syncwarp();
+        uint32_t Orun = 0;
+        for (uint32_t ci = 0; ci < nch; ci++) {
+          const uint32_t pos = ci * 32 + lane;
+          const bool valid = pos < len;
+          const uint32_t rr = valid ? (uint32_t)src[pos] : 0u;
+          const bool P1 = valid && (rr & bitmask);
+          const uint32_t m = __ballot_sync(FULL, P1);
+          if (lane == 0) ws.LB[ci] = m;
+          if (do_split) {
+            const uint32_t Y = Orun + __popc(m & lt);
+            const uint32_t tb = ws.T[rr >> bitsh];
+            const uint32_t d = P1 ? tb + Y : tb + pos - Y;
+            if (valid) {
+              if (HAS_OUT && k + 1 == tau) ko[rs + d] = (OutT)(rr & pmask);
+              else dst[d] = (RecT)rr;
+            }
+            Orun += __popc(m);
+          }
+        }
+        __syncwarp();
+        // the row's level bits are LB[0..len) in order: copy into the batch staging
+        if (lane == 0) {
+          for (uint32_t ci = 0; ci < nch; ci++) {
+            const uint32_t nb = min(32u, len - ci * 32);
+            const uint32_t v = nb == 32 ? ws.LB[ci] : (ws.LB[ci] & ((1u << nb) - 1u));
+            stage_bits(ws.SB[k], soff + ci * 32, v);
+          }
+        }
+        __syncwarp();
+      }
+      }
+    }
+    if (COUNT) {
+      if (lane < (int)p.nk) p.batchcnt[(uint64_t)lane * p.nbatch + b] = nodeoff;
+      continue;
+    }
+    __syncwarp();
+    // ---- the batch's bits [A, Bend) of each level -> global; only edge words shared ----
+    for (uint32_t k = 0; k < tau; k++) {
+      uint64_t *Bw = p.bits + (uint64_t)(p.l0 + k) * p.wpl;
+      const uint64_t g0 = A >> 6, g1 = ((uint64_t)Bend - 1) >> 6;
+      for (uint64_t gw = g0 + lane; gw <= g1; gw += 32) {
+        // 64 bits of staging starting at local bit (gw*64 - A)
+        const int base = (int)((int64_t)gw * 64 - (int64_t)A);
+        uint64_t v = extract64(ws.SB[k], base, (int)nsw);
+        const uint64_t lo = gw * 64, hi = lo + 64;
+        const uint64_t s0 = (uint64_t)A > lo ? (uint64_t)A - lo : 0;
+        const uint64_t e0 = (uint64_t)Bend < hi ? (uint64_t)Bend - lo : 64;
+        v &= (e0 - s0 == 64) ? ~0ull : (((1ull << (e0 - s0)) - 1ull) << s0);
+        const uint64_t hi_clip = hi < p.n ? hi : p.n;
+        if ((uint64_t)A <= lo && (uint64_t)Bend >= hi_clip) Bw[gw] = v;
+        else if (v) atomicOr(reinterpret_cast<unsigned long long *>(&Bw[gw]), (unsigned long long)v);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Batches: batch b = the rows whose start lies in [b*TW, (b+1)*TW).
+// batch_first[b] = lower_bound(row_start, b*TW), b = 0..nbatch.
+__global__ void k_batches(const uint32_t *__restrict__ row_start, const uint32_t *__restrict__ counts,
+                          uint32_t nbatch, uint32_t *__restrict__ batch_first, uint32_t *__restrict__ bcounts,
+                          const uint32_t *err) {
+  if (*err) return;
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) bcounts[1] = nbatch;  // "rows" of the batch-count scan
+  if (b > nbatch) return;
+  const uint32_t nr = counts[1];
+  const uint64_t key = (uint64_t)b * TW;
+  uint32_t lo = 0, hi = nr;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (row_start[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  batch_first[b] = b == nbatch ? nr : lo;
+}
+
+// Rows of a local-mode group = the non-empty nodes of level l0 (grid-stride).
+__global__ void k_rows_from_nodes(const uint64_t *__restrict__ level_node_ptr, const uint32_t *__restrict__ ncount,
+                                  uint32_t l0, const uint32_t *__restrict__ node_key,
+                                  const uint32_t *__restrict__ node_start, uint32_t *__restrict__ row_start,
+                                  uint32_t *__restrict__ row_key, uint32_t *__restrict__ counts, const uint32_t *err) {
+  if (*err) return;
+  const uint64_t p0 = level_node_ptr[l0];
+  const uint32_t nr = ncount[l0];
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[1] = nr;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x) {
+    row_start[r] = node_start[p0 + r];
+    row_key[r] = node_key[p0 + r];
+  }
+}
+
+}  // namespace wtb

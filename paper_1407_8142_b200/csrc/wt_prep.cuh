@@ -190,67 +190,199 @@ __global__ void k_row_scan(const uint32_t *__restrict__ E, uint32_t stride, cons
 }
 
 // ---------------------------------------------------------------------------
-// A4: non-empty nodes of levels l0+k (k = k_lo .. k_hi) from the rows' Cseg.
-// Node (P << k | q) is non-empty iff Cseg[r][(q+1) << (tau-k)] > Cseg[r][q << (tau-k)]
-// (Fig. 1 l.18-20).  One CTA per level; rows in order, so keys ascend.
+// A4: non-empty nodes of the group's levels l0+k (k = k_lo .. k_hi).  Node
+// (P << k | q) of row r is non-empty iff its count is > 0 (Fig. 1 l.18-20);
+// rows are in key order, so the CSR order is (level, row, q).  Three steps,
+// all multi-CTA so that millions of rows scale:
+//   k_row_nodes_count  rowcnt[k][r] = non-empty q of row r at level l0+k
+//                      (from Cseg, chain mode)
+//   k_scan_rows        exclusive scan of rowcnt per level (two-level scan),
+//                      ncount[l0+k] = level total, level_node_ptr
+//   k_row_nodes_emit   writes (key, start) at base + rowoff + local rank
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool node_nonempty(const uint32_t *Cs, uint32_t ndig, uint32_t r, uint32_t q,
-                                              uint32_t sh) {
-  const uint32_t *row = Cs + (uint64_t)r * (ndig + 1);
-  return row[(q + 1) << sh] > row[q << sh];
+__global__ void k_row_nodes_count(const uint32_t *__restrict__ Cseg, const uint32_t *__restrict__ counts,
+                                  uint32_t tau, uint32_t k_lo, uint32_t nk, uint64_t rstride,
+                                  uint32_t *__restrict__ rowcnt, const uint32_t *err) {
+  if (*err) return;
+  const uint32_t nr = counts[1], ndig = 1u << tau;
+  const uint64_t items = (uint64_t)nr * nk;
+  for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(it % nr), kk = (uint32_t)(it / nr);
+    const uint32_t k = k_lo + kk, sh = tau - k;
+    const uint32_t *row = Cseg + (uint64_t)r * (ndig + 1);
+    uint32_t c = 0;
+    for (uint32_t q = 0; q < (1u << k); q++) c += row[(q + 1) << sh] > row[q << sh];
+    rowcnt[(uint64_t)kk * rstride + r] = c;
+  }
 }
 
-__global__ void __launch_bounds__(1024) k_nodes_count(const uint32_t *__restrict__ Cseg,
-                                                     const uint32_t *__restrict__ counts, uint32_t tau, uint32_t l0,
-                                                     uint32_t k_lo, uint32_t *__restrict__ ncount,
-                                                     const uint32_t *err) {
+constexpr int SCAN_BLK = 2048;  // rows per scan block
+
+// pass 1: per (level, block) sums.  grid (nblocks, nk), 1024 threads.
+__global__ void __launch_bounds__(1024) k_scan_rows_1(const uint32_t *__restrict__ rowcnt, uint64_t rstride,
+                                                     const uint32_t *__restrict__ counts, uint32_t *__restrict__ bsum,
+                                                     uint32_t bstride, const uint32_t *err) {
   __shared__ uint32_t shm[33];
   if (*err) return;
-  const uint32_t k = k_lo + blockIdx.x;
-  const uint32_t nr = counts[1], nq = 1u << k, sh = tau - k, ndig = 1u << tau;
-  const uint64_t tot_items = (uint64_t)nr * nq;
-  uint32_t c = 0;
-  for (uint64_t f = threadIdx.x; f < tot_items; f += blockDim.x)
-    c += node_nonempty(Cseg, ndig, (uint32_t)(f >> k), (uint32_t)(f & (nq - 1)), sh);
+  const uint32_t nr = counts[1];
+  const uint64_t b0 = (uint64_t)blockIdx.x * SCAN_BLK;
+  if (b0 >= nr) return;
+  const uint32_t *rc = rowcnt + (uint64_t)blockIdx.y * rstride;
+  uint32_t s = 0;
+  for (uint64_t r = b0 + threadIdx.x; r < b0 + SCAN_BLK && r < nr; r += blockDim.x) s += rc[r];
   uint32_t tot;
-  block_exscan(c, shm, &tot);
-  if (threadIdx.x == 0) ncount[l0 + k] = tot;
+  block_exscan(s, shm, &tot);
+  if (threadIdx.x == 0) bsum[(uint64_t)blockIdx.y * bstride + blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(1024) k_nodes_emit(const uint32_t *__restrict__ Cseg,
-                                                    const uint32_t *__restrict__ counts, uint32_t tau, uint32_t l0,
-                                                    uint32_t k_lo, uint32_t L, const uint32_t *__restrict__ row_key,
-                                                    const uint32_t *__restrict__ row_start,
-                                                    const uint32_t *__restrict__ ncount,
-                                                    uint64_t *__restrict__ level_node_ptr,
-                                                    uint32_t *__restrict__ node_key,
-                                                    uint32_t *__restrict__ node_start, const uint32_t *err) {
+// pass 2: per level, exclusive scan of the block sums (one CTA per level);
+// also the level totals, their CSR bases and level_node_ptr.
+__global__ void __launch_bounds__(1024) k_scan_rows_2(uint32_t *__restrict__ bsum, uint32_t bstride,
+                                                     const uint32_t *__restrict__ counts, uint32_t l0, uint32_t k_lo,
+                                                     uint32_t nk, uint32_t L, uint32_t *__restrict__ ncount,
+                                                     uint64_t *__restrict__ level_node_ptr, const uint32_t *err) {
   __shared__ uint32_t shm[33];
   if (*err) return;
-  const uint32_t k = k_lo + blockIdx.x;
-  const uint32_t lev = l0 + k;
-  uint64_t base = 0;
-  for (uint32_t l = 0; l < lev; l++) base += ncount[l];
-  if (threadIdx.x == 0) {
+  const uint32_t nr = counts[1];
+  const uint32_t nb = (nr + SCAN_BLK - 1) / SCAN_BLK;
+  uint32_t *bs = bsum + (uint64_t)blockIdx.x * bstride;
+  uint32_t carry = 0;
+  for (uint32_t b0 = 0; b0 < nb; b0 += blockDim.x) {
+    const uint32_t b = b0 + threadIdx.x;
+    const uint32_t v = b < nb ? bs[b] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_exscan(v, shm, &tot);
+    if (b < nb) bs[b] = carry + ex;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ncount[l0 + k_lo + blockIdx.x] = carry;
+}
+
+// Level CSR bases: level_node_ptr[lev] for the group's levels (runs after pass 2).
+__global__ void k_level_ptr(const uint32_t *__restrict__ ncount, uint32_t l0, uint32_t k_lo, uint32_t nk, uint32_t L,
+                            uint64_t *__restrict__ level_node_ptr, const uint32_t *err) {
+  if (*err) return;
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (uint32_t kk = 0; kk < nk; kk++) {
+    const uint32_t lev = l0 + k_lo + kk;
+    uint64_t base = 0;
+    for (uint32_t l = 0; l < lev; l++) base += ncount[l];
     level_node_ptr[lev] = base;
     if (lev + 1 == L) level_node_ptr[L] = base + ncount[lev];
   }
-  const uint32_t nr = counts[1], nq = 1u << k, sh = tau - k, ndig = 1u << tau;
-  const uint64_t tot_items = (uint64_t)nr * nq;
-  uint64_t carry = 0;
-  for (uint64_t f0 = 0; f0 < tot_items; f0 += blockDim.x) {
-    const uint64_t f = f0 + threadIdx.x;
-    const uint32_t r = (uint32_t)(f >> k), q = (uint32_t)(f & (nq - 1));
-    const bool ne = f < tot_items && node_nonempty(Cseg, ndig, r, q, sh);
+}
+
+// pass 3: rowoff[k][r] = exclusive prefix within the level (in place over rowcnt).
+__global__ void __launch_bounds__(1024) k_scan_rows_3(uint32_t *__restrict__ rowcnt, uint64_t rstride,
+                                                     const uint32_t *__restrict__ counts,
+                                                     const uint32_t *__restrict__ bsum, uint32_t bstride,
+                                                     const uint32_t *err) {
+  __shared__ uint32_t shm[33];
+  if (*err) return;
+  const uint32_t nr = counts[1];
+  const uint64_t b0 = (uint64_t)blockIdx.x * SCAN_BLK;
+  if (b0 >= nr) return;
+  uint32_t *rc = rowcnt + (uint64_t)blockIdx.y * rstride;
+  uint32_t carry = bsum[(uint64_t)blockIdx.y * bstride + blockIdx.x];
+  for (uint64_t base = b0; base < b0 + SCAN_BLK && base < nr; base += blockDim.x) {
+    const uint64_t r = base + threadIdx.x;
+    const bool in = r < b0 + SCAN_BLK && r < nr;
+    const uint32_t v = in ? rc[r] : 0u;
     uint32_t tot;
-    const uint32_t off = block_exscan(ne ? 1u : 0u, shm, &tot);
-    if (ne) {
-      const uint64_t j = base + carry + off;
-      node_key[j] = (row_key[r] << k) | q;
-      node_start[j] = row_start[r] + Cseg[(uint64_t)r * (ndig + 1) + (q << sh)];
-    }
+    const uint32_t ex = block_exscan(v, shm, &tot);
+    if (in) rc[r] = carry + ex;
     carry += tot;
     __syncthreads();
+  }
+}
+
+__global__ void k_row_nodes_emit(const uint32_t *__restrict__ Cseg, const uint32_t *__restrict__ counts, uint32_t tau,
+                                 uint32_t l0, uint32_t k_lo, uint32_t nk, uint64_t rstride,
+                                 const uint32_t *__restrict__ rowoff, const uint64_t *__restrict__ level_node_ptr,
+                                 const uint32_t *__restrict__ row_key, const uint32_t *__restrict__ row_start,
+                                 uint32_t *__restrict__ node_key, uint32_t *__restrict__ node_start,
+                                 const uint32_t *err) {
+  if (*err) return;
+  const uint32_t nr = counts[1], ndig = 1u << tau;
+  const uint64_t items = (uint64_t)nr * nk;
+  for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(it % nr), kk = (uint32_t)(it / nr);
+    const uint32_t k = k_lo + kk, sh = tau - k;
+    const uint32_t *row = Cseg + (uint64_t)r * (ndig + 1);
+    uint64_t j = level_node_ptr[l0 + k] + rowoff[(uint64_t)kk * rstride + r];
+    const uint32_t P = row_key[r], rs = row_start[r];
+    for (uint32_t q = 0; q < (1u << k); q++) {
+      const uint32_t a = row[q << sh], b = row[(q + 1) << sh];
+      if (b > a) {
+        node_key[j] = (P << k) | q;
+        node_start[j] = rs + a;
+        j++;
+      }
+    }
+  }
+}
+
+// Occupancy of the 2^tau digits of a row as 8 words (bit i of word j = digit
+// 32j + i), reduced level by level: a level-(k-1) prefix is non-empty iff one
+// of its two children is.  Returns the occupancy popcount per level in cnt[k].
+__device__ __forceinline__ uint32_t gather_pairs(uint32_t w) {  // OR bit pairs, pack 16 bits
+  w = (w | (w >> 1)) & 0x55555555u;
+  w = (w | (w >> 1)) & 0x33333333u;
+  w = (w | (w >> 2)) & 0x0f0f0f0fu;
+  w = (w | (w >> 4)) & 0x00ff00ffu;
+  w = (w | (w >> 8)) & 0x0000ffffu;
+  return w;
+}
+
+// Local mode (rows small enough for one tile): per-row node counts straight
+// from the row's keys.  One warp per row; a row larger than TW sets err |= 2
+// (the host then rebuilds with chain mode).
+template <typename KeyT>
+__global__ void __launch_bounds__(256) k_local_count(const KeyT *__restrict__ keys, uint32_t pbits, uint32_t tau,
+                                                    uint32_t nk, const uint32_t *__restrict__ chain_begin,
+                                                    const uint32_t *__restrict__ chain_end,
+                                                    const uint32_t *__restrict__ counts, uint64_t rstride,
+                                                    uint32_t *__restrict__ rowcnt, uint32_t *err) {
+  __shared__ uint32_t h[8][NDIG];
+  if (ld_relaxed(err)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t nr = counts[1], ndig = 1u << tau;
+  for (uint32_t r = blockIdx.x * 8 + warp; r < nr; r += gridDim.x * 8) {
+    const uint32_t beg = chain_begin[r], end = chain_end[r];
+    if (end - beg > (uint32_t)TW) {
+      if (lane == 0) atomicOr(err, 2u);
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < NDIG / 32; i++) h[warp][lane + 32 * i] = 0;
+    __syncwarp();
+    for (uint32_t i = beg + lane; i < end; i += 32) h[warp][((uint32_t)keys[i] >> pbits) & (ndig - 1u)] = 1u;
+    __syncwarp();
+    uint32_t w[NDIG / 32];
+#pragma unroll
+    for (int j = 0; j < NDIG / 32; j++) w[j] = __ballot_sync(FULL, h[warp][32 * j + lane] != 0);
+    // level k = tau: w holds 2^tau bits; reduce to k = tau-1, ..., 1
+    uint32_t nbits = ndig;
+    for (int k = (int)tau; k >= 1; k--) {
+      if ((uint32_t)k <= nk && lane == 0) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 0; j < NDIG / 32; j++) c += (32u * j < nbits) ? __popc(w[j]) : 0u;
+        rowcnt[(uint64_t)(k - 1) * rstride + r] = c;
+      }
+      // halve: word j' = pairs of words 2j', 2j'+1
+      uint32_t nw[NDIG / 32];
+#pragma unroll
+      for (int j = 0; j < NDIG / 64; j++) nw[j] = gather_pairs(w[2 * j]) | (gather_pairs(w[2 * j + 1]) << 16);
+#pragma unroll
+      for (int j = NDIG / 64; j < NDIG / 32; j++) nw[j] = 0;
+      if (nbits <= 32) nw[0] = gather_pairs(w[0]);
+#pragma unroll
+      for (int j = 0; j < NDIG / 32; j++) w[j] = nw[j];
+      nbits >>= 1;
+    }
+    __syncwarp();
   }
 }
 

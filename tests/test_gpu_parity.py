@@ -165,3 +165,56 @@ def test_full_config_vs_oracle(cfg_idx):
     cfg = gen.CONFIGS[cfg_idx]
     S = gen.config_input(cfg)
     _compare(S, cfg.sigma)
+
+
+# ---- L > 16: four groups, narrowed u32/u16/u8 keys, local mode for small nodes ----
+@pytest.mark.parametrize("sigma", [1 << 17, 3 << 18, 1 << 20, 1 << 24, (1 << 31) + 5, 1 << 32])
+@pytest.mark.parametrize("n", [1, 4097, 100000, 1 << 20])
+def test_large_alphabet(n, sigma):
+    S = gen.uniform_below(n, sigma, seed=n + (sigma & 0xFFFF), dtype=np.uint32)
+    _compare(S, sigma)
+
+
+@pytest.mark.parametrize("sigma", [1 << 20, 1 << 32])
+def test_large_alphabet_adversarial(sigma):
+    n = 60000
+    _compare(np.full(n, sigma - 1, dtype=np.uint32), sigma)           # one huge node per level
+    S = gen.uniform_below(n, 64, seed=2, dtype=np.uint32) * np.uint32(sigma // 64)
+    _compare(S, sigma)                                                # few, large deep nodes
+    S = np.sort(gen.uniform_below(n, sigma, seed=4, dtype=np.uint32))
+    _compare(S, sigma)
+
+
+def test_large_alphabet_queries():
+    wt = _wt()
+    n, sigma = 200000, 1 << 32
+    S = gen.uniform_below(n, sigma, seed=77, dtype=np.uint32)
+    S[1000:1100] = S[5]  # a repeated symbol
+    tree = wt.build(torch.from_numpy(S).cuda(), sigma)
+    pos = np.random.default_rng(3).integers(0, n, 3000)
+    got = tree.access(torch.from_numpy(pos).cuda()).cpu().numpy()
+    assert np.array_equal(got, S[pos])
+    cs = S[pos[:500]].astype(np.int64).astype(np.int32)  # u32 symbols through an int32 view
+    r = tree.rank(torch.from_numpy(cs).cuda(), torch.from_numpy(pos[:500]).cuda()).cpu().numpy()
+    want = [pins.rank_bruteforce(S, np.uint32(c), i) for c, i in zip(S[pos[:500]], pos[:500])]
+    assert r.tolist() == want
+    tree.free()
+
+
+@pytest.mark.slow
+def test_full_config5_vs_oracle():
+    """Config 5 (n = 2^29 u32, sigma = 2^32, 32 levels, ~1.7e9 nodes) at full
+    size: every array bit-exact, compared one array at a time (host RAM)."""
+    wt = _wt()
+    cfg = gen.CONFIGS[5]
+    S = gen.config_input(cfg)
+    with oracle.OracleTree(S, cfg.sigma) as ot:
+        tree = wt.build(torch.from_numpy(S).cuda(), cfg.sigma)
+        assert tree.total_nodes == ot.total_nodes
+        for k in KEYS:
+            want = ot.array(k)
+            got = getattr(tree, k).cpu().numpy()
+            assert got.shape == want.shape, k
+            assert np.array_equal(got, want), f"{k} differs"
+            del want, got
+        tree.free()
