@@ -81,6 +81,23 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t *shm, uint
   return shm[warp] + incl - v;
 }
 
+// Explicit shared-memory (state space .shared) accesses by 32-bit byte address.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <typename T>
+__device__ __forceinline__ uint32_t lds(uint32_t a) {
+  uint32_t v;
+  if constexpr (sizeof(T) == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  else if constexpr (sizeof(T) == 2) asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+  else asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
+  if constexpr (sizeof(T) == 1) asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+  else if constexpr (sizeof(T) == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+  else asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 // Bits [base, base+64) of a little-endian bit array of nw u32 words; bits
 // outside [0, 32*nw) read as 0.  base may be negative (> -64).
 __device__ __forceinline__ uint64_t extract64(const uint32_t *w, int base, int nw) {

@@ -165,10 +165,9 @@ GroupLaunch group_launch() {
   static std::once_flag f;
   std::call_once(f, [] {
     gl.kern = k_group<InT, RecT, OutT, HAS_OUT>;
-    gl.smem = GROUP_WARPS * sizeof(WarpSmem<RecT>);
-    cudaFuncSetAttribute(gl.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gl.smem);
+    gl.smem = 0;  // static shared memory, one warp per CTA
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl.kern, GROUP_WARPS * 32, gl.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl.kern, 32, 0);
     gl.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
   });
   return gl;
@@ -363,7 +362,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       gb.nbatch = (uint32_t)((n + TW - 1) / TW);
       gb.max_chains = 1;
     } else {
-      const uint64_t warps = (uint64_t)gb.gl.grid * GROUP_WARPS;
+      const uint64_t warps = (uint64_t)gb.gl.grid;  // one warp per CTA
       static const uint64_t cpw =
           getenv("WT_CHAINS_PER_WARP") ? strtoull(getenv("WT_CHAINS_PER_WARP"), 0, 10) : 8;
       const uint64_t target = (n + cpw * warps - 1) / (cpw * warps);
@@ -575,7 +574,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     char name[32];
     snprintf(name, sizeof(name), "k_group%u", g);
     rec.begin(name, n * gb.inw + (has_out ? n * gb.outw : 0) + (uint64_t)gb.tau * n / 8);
-    gb.gl.kern<<<gb.gl.grid, GROUP_WARPS * 32, gb.gl.smem, s>>>(gp);
+    gb.gl.kern<<<gb.gl.grid, 32, 0, s>>>(gp);
     chk(cudaGetLastError());
     rec.end();
     keys_in = gb.keys_out;

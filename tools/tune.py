@@ -8,10 +8,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
-    "tw4k_w2": ["WT_TW=4096", "WT_GROUP_WARPS=2"],
-    "tw4k_w1": ["WT_TW=4096", "WT_GROUP_WARPS=1"],
-    "tw2k_w2": ["WT_TW=2048", "WT_GROUP_WARPS=2"],
-    "tw8k_w1": ["WT_TW=8192", "WT_GROUP_WARPS=1"],
+    "gtw2k": ["WT_GTW=2048"],
+    "gtw1k": ["WT_GTW=1024"],
+    "gtw4k": ["WT_GTW=4096"],
 }
 CPW = os.environ.get("TUNE_CPW", "3").split(",")
 if sys.argv[1] == "build":
