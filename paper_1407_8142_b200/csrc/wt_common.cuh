@@ -17,6 +17,23 @@ constexpr uint32_t FLAG_AGG = 1u << 30;  // lookback: tile aggregate published
 constexpr uint32_t FLAG_INC = 2u << 30;  // lookback: inclusive prefix published
 constexpr uint32_t VAL_MASK = (1u << 30) - 1;
 
+#ifdef WT_DEBUG
+__device__ uint32_t g_wt_dbg[4];
+#define WT_CHECK(cond, code)                                                        \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      if (atomicCAS(&::wtb::g_wt_dbg[0], 0u, (uint32_t)(code)) == 0u) {             \
+        ::wtb::g_wt_dbg[1] = blockIdx.x;                                            \
+        ::wtb::g_wt_dbg[2] = threadIdx.x;                                           \
+      }                                                                             \
+    }                                                                               \
+  } while (0)
+#else
+#define WT_CHECK(cond, code) \
+  do {                       \
+  } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -96,6 +113,10 @@ __device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
   if constexpr (sizeof(T) == 1) asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
   else if constexpr (sizeof(T) == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
   else asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 
 // Bits [base, base+64) of a little-endian bit array of nw u32 words; bits

@@ -157,6 +157,7 @@ struct GroupLaunch {
   void (*kern)(GroupParams) = nullptr;
   size_t smem = 0;
   int grid = 0;
+  uint32_t tile = 0;  // positions per tile (chains are cut at multiples of it)
 };
 
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
@@ -165,9 +166,10 @@ GroupLaunch group_launch() {
   static std::once_flag f;
   std::call_once(f, [] {
     gl.kern = k_group<InT, RecT, OutT, HAS_OUT>;
-    gl.smem = 0;  // static shared memory, one warp per CTA
+    gl.smem = 0;  // static shared memory
+    gl.tile = GroupTile<RecT>::TT;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl.kern, 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl.kern, WPB * 32, 0);
     gl.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
   });
   return gl;
@@ -362,11 +364,12 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       gb.nbatch = (uint32_t)((n + TW - 1) / TW);
       gb.max_chains = 1;
     } else {
-      const uint64_t warps = (uint64_t)gb.gl.grid;  // one warp per CTA
+      const uint64_t warps = (uint64_t)gb.gl.grid;  // CTAs (one chain at a time each)
       static const uint64_t cpw =
           getenv("WT_CHAINS_PER_WARP") ? strtoull(getenv("WT_CHAINS_PER_WARP"), 0, 10) : 8;
       const uint64_t target = (n + cpw * warps - 1) / (cpw * warps);
-      gb.CH = std::max<uint64_t>(TW, ((target + TW - 1) / TW) * TW);
+      const uint64_t tt = gb.gl.tile;
+      gb.CH = std::max<uint64_t>(tt, ((target + tt - 1) / tt) * tt);
       gb.max_chains = g == 0 ? std::max<uint64_t>((n + gb.CH - 1) / gb.CH, 1)
                              : (n + gb.CH - 1) / gb.CH + gb.max_rows;
     }
@@ -574,7 +577,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     char name[32];
     snprintf(name, sizeof(name), "k_group%u", g);
     rec.begin(name, n * gb.inw + (has_out ? n * gb.outw : 0) + (uint64_t)gb.tau * n / 8);
-    gb.gl.kern<<<gb.gl.grid, 32, 0, s>>>(gp);
+    gb.gl.kern<<<gb.gl.grid, WPB * 32, 0, s>>>(gp);
     chk(cudaGetLastError());
     rec.end();
     keys_in = gb.keys_out;
@@ -704,5 +707,23 @@ int wt_last_profile(wt_profile *out) {
 }
 
 const char *wt_version(void) { return "wt-b200 0.1 (sm_100a)"; }
+
+#ifdef WT_PHASES
+int wt_phases(unsigned long long *out16) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, wtb::g_ph, 16 * sizeof(unsigned long long));
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(wtb::g_ph, z, sizeof(z));
+  return WT_OK;
+}
+#endif
+
+#ifdef WT_DEBUG
+int wt_debug_code(uint32_t *out4) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out4, wtb::g_wt_dbg, 4 * sizeof(uint32_t));
+  return WT_OK;
+}
+#endif
 
 }  // extern "C"

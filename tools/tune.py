@@ -8,9 +8,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
-    "gtw2k": ["WT_GTW=2048"],
-    "gtw1k": ["WT_GTW=1024"],
-    "gtw4k": ["WT_GTW=4096"],
+    "minb6": ["WT_GMINB=6"],
+    "minb5": ["WT_GMINB=5"],
+    "minb4_tt8k": ["WT_GMINB=4", "WT_GTT=8192"],
 }
 CPW = os.environ.get("TUNE_CPW", "3").split(",")
 if sys.argv[1] == "build":
