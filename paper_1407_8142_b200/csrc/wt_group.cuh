@@ -86,7 +86,7 @@ __device__ unsigned long long g_ph[16];
 constexpr int WPB = 4;  // warps per CTA
 constexpr int J0 = 2;   // levels split by the whole CTA (log2 WPB)
 #ifndef WT_GMINB
-#define WT_GMINB 4
+#define WT_GMINB 5
 #endif
 #ifndef WT_GTT
 #define WT_GTT 8192
