@@ -41,19 +41,21 @@ struct Recorder {
   bool timed;
   std::vector<Launch> launches;
   explicit Recorder(cudaStream_t st, bool t) : s(st), timed(t) {}
-  void begin(const char *name, uint64_t bytes) {
+  cudaStream_t cur = nullptr;
+  void begin(const char *name, uint64_t bytes, cudaStream_t on = nullptr) {
     Launch L;
     L.name = name;
     L.algo_bytes = bytes;
+    cur = on ? on : s;
     if (timed) {
       cudaEventCreate(&L.e0);
       cudaEventCreate(&L.e1);
-      cudaEventRecord(L.e0, s);
+      cudaEventRecord(L.e0, cur);
     }
     launches.push_back(L);
   }
   void end() {
-    if (timed) cudaEventRecord(launches.back().e1, s);
+    if (timed) cudaEventRecord(launches.back().e1, cur);
   }
   void publish() {  // after the stream has been synchronised
     wt_profile p{};
@@ -100,6 +102,15 @@ uint32_t levels_of(uint64_t sigma) {
   uint32_t L = 0;
   while (v) { L++; v >>= 1; }
   return L;
+}
+
+// A second stream of the same device for the rank directory of finished
+// level groups, so that it overlaps the next group pass (created once).
+cudaStream_t side_stream() {
+  static cudaStream_t side = nullptr;
+  static std::once_flag f;
+  std::call_once(f, [] { cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking); });
+  return side;
 }
 
 int g_num_sms = 0;
@@ -405,6 +416,26 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   if (L && n) chk(cudaMemsetAsync(t->bits, 0, L * WPL * sizeof(uint64_t), s));
   for (uint32_t g = 0; g < NG; g++) chk(cudaMemsetAsync(G[g].counts, 0, 4 * sizeof(uint32_t), s));
 
+  // A7 per level group, on the side stream once the group's bitmaps are final
+  cudaStream_t side = side_stream();
+  cudaEvent_t ev_side = nullptr;
+  bool side_used = false;
+  auto rank_levels = [&](uint32_t lbeg, uint32_t nl) {
+    if (!NSD || !nl || !n) return;
+    cudaEvent_t ev;
+    chk(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    chk(cudaEventRecord(ev, s));
+    chk(cudaStreamWaitEvent(side, ev, 0));
+    cudaEventDestroy(ev);
+    const uint64_t warps = (uint64_t)nl * NSD;
+    rec.begin("k_rank_local", nl * WPL * 8 + nl * BPL * 2 + nl * NSD * 8, side);
+    k_rank_local<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, side>>>(t->bits, WPL, BPL, NSD, lbeg, nl,
+                                                                           t->rank_block, suptot, err);
+    chk(cudaGetLastError());
+    rec.end();
+    side_used = true;
+  };
+
   const void *keys_in = seq;
   for (uint32_t g = 0; g < NG || (g == 0 && L == 0); g++) {
     // ---- chains of this group + their digit histograms (A1 for g = 0) ----
@@ -494,6 +525,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       gb.ll.build<<<gb.ll.grid, LOCAL_WARPS * 32, gb.ll.smem, s>>>(lp);
       chk(cudaGetLastError());
       rec.end();
+      rank_levels(gb.l0, gb.tau);
       keys_in = gb.keys_out;
       continue;
     } else {
@@ -534,7 +566,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     // ---- A4: node table of this group's levels l0+k_lo .. l0+k_lo+nk-1 ----
     if (gb.nk) {
       const uint64_t rstride = gb.max_rows;
-      const unsigned cgrid = (unsigned)std::min<uint64_t>((gb.max_rows * gb.nk + 255) / 256, 65535);
+      const unsigned cgrid = (unsigned)std::min<uint64_t>((gb.max_rows * gb.nk * 32 + 255) / 256, 65535);
       rec.begin("k_nodes_count", 0);
       k_row_nodes_count<<<cgrid, 256, 0, s>>>(gb.Cseg, gb.counts, gb.tau, gb.k_lo, gb.nk, rstride, gb.rowcnt, err);
       chk(cudaGetLastError());
@@ -580,18 +612,16 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     gb.gl.kern<<<gb.gl.grid, WPB * 32, 0, s>>>(gp);
     chk(cudaGetLastError());
     rec.end();
+    rank_levels(gb.l0, gb.tau);
     keys_in = gb.keys_out;
   }
 
   if (L > 0 && n > 0) {
-    // ---- A7: rank directory from the finished bitmaps ----
-    if (NSD) {
-      const uint64_t warps = (uint64_t)L * NSD;
-      rec.begin("k_rank_local", L * WPL * 8 + L * BPL * 2 + L * NSD * 8);
-      k_rank_local<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(t->bits, WPL, BPL, NSD, L, t->rank_block,
-                                                                        suptot, err);
-      chk(cudaGetLastError());
-      rec.end();
+    // ---- A7: rank directory (per-group block counts ran on the side stream) ----
+    if (side_used) {
+      chk(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
+      chk(cudaEventRecord(ev_side, side));
+      chk(cudaStreamWaitEvent(s, ev_side, 0));
     }
     rec.begin("k_rank_super", L * SPL * 16);
     k_rank_super<<<L, 1024, 0, s>>>(suptot, NSD, SPL, t->rank_super, err);
@@ -602,6 +632,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     chk(cudaMemsetAsync(t->rank_super, 0, L * SPL * sizeof(uint64_t), s));
   }
 
+  if (ev_side) cudaEventDestroy(ev_side);
   // ---- the single host sync: error flag + node count ----
   chk(cudaMemcpyAsync(h_stage, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   if (L) chk(cudaMemcpyAsync(h_stage + 1, t->level_node_ptr + L, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));

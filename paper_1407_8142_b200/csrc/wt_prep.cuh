@@ -203,16 +203,23 @@ __global__ void k_row_scan(const uint32_t *__restrict__ E, uint32_t stride, cons
 __global__ void k_row_nodes_count(const uint32_t *__restrict__ Cseg, const uint32_t *__restrict__ counts,
                                   uint32_t tau, uint32_t k_lo, uint32_t nk, uint64_t rstride,
                                   uint32_t *__restrict__ rowcnt, const uint32_t *err) {
+  // one warp per (row, level): lanes test 32 prefixes q at a time
   if (*err) return;
   const uint32_t nr = counts[1], ndig = 1u << tau;
+  const int lane = threadIdx.x & 31;
   const uint64_t items = (uint64_t)nr * nk;
-  for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (uint64_t)gridDim.x * blockDim.x) {
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nwarps) {
     const uint32_t r = (uint32_t)(it % nr), kk = (uint32_t)(it / nr);
     const uint32_t k = k_lo + kk, sh = tau - k;
     const uint32_t *row = Cseg + (uint64_t)r * (ndig + 1);
     uint32_t c = 0;
-    for (uint32_t q = 0; q < (1u << k); q++) c += row[(q + 1) << sh] > row[q << sh];
-    rowcnt[(uint64_t)kk * rstride + r] = c;
+    for (uint32_t q0 = 0; q0 < (1u << k); q0 += 32) {
+      const uint32_t q = q0 + lane;
+      const bool ne = q < (1u << k) && row[(q + 1) << sh] > row[q << sh];
+      c += __popc(__ballot_sync(FULL, ne));
+    }
+    if (lane == 0) rowcnt[(uint64_t)kk * rstride + r] = c;
   }
 }
 
@@ -303,22 +310,33 @@ __global__ void k_row_nodes_emit(const uint32_t *__restrict__ Cseg, const uint32
                                  const uint32_t *__restrict__ row_key, const uint32_t *__restrict__ row_start,
                                  uint32_t *__restrict__ node_key, uint32_t *__restrict__ node_start,
                                  const uint32_t *err) {
+  // one warp per (row, level); node j = level base + row offset + rank among the row's non-empty q
   if (*err) return;
   const uint32_t nr = counts[1], ndig = 1u << tau;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
   const uint64_t items = (uint64_t)nr * nk;
-  for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (uint64_t)gridDim.x * blockDim.x) {
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nwarps) {
     const uint32_t r = (uint32_t)(it % nr), kk = (uint32_t)(it / nr);
     const uint32_t k = k_lo + kk, sh = tau - k;
     const uint32_t *row = Cseg + (uint64_t)r * (ndig + 1);
     uint64_t j = level_node_ptr[l0 + k] + rowoff[(uint64_t)kk * rstride + r];
     const uint32_t P = row_key[r], rs = row_start[r];
-    for (uint32_t q = 0; q < (1u << k); q++) {
-      const uint32_t a = row[q << sh], b = row[(q + 1) << sh];
-      if (b > a) {
-        node_key[j] = (P << k) | q;
-        node_start[j] = rs + a;
-        j++;
+    for (uint32_t q0 = 0; q0 < (1u << k); q0 += 32) {
+      const uint32_t q = q0 + lane;
+      uint32_t a = 0, b = 0;
+      if (q < (1u << k)) {
+        a = row[q << sh];
+        b = row[(q + 1) << sh];
       }
+      const uint32_t bm = __ballot_sync(FULL, b > a);
+      if (b > a) {
+        const uint64_t jj = j + __popc(bm & lt);
+        node_key[jj] = (P << k) | q;
+        node_start[jj] = rs + a;
+      }
+      j += __popc(bm);
     }
   }
 }

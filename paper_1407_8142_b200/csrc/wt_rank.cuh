@@ -14,15 +14,16 @@ namespace wtb {
 // k_rank_local: one warp per (level, superblock); k_rank_super: one CTA per level.
 // ---------------------------------------------------------------------------
 __global__ void k_rank_local(const uint64_t *__restrict__ bits, uint64_t wpl, uint64_t bpl, uint64_t nsup_data,
-                             uint32_t L, uint16_t *__restrict__ rank_block, uint64_t *__restrict__ suptot,
-                             const uint32_t *err) {
-  // One warp per (level, superblock): popcount of its <= 128 blocks of 8 words
-  // (a streaming read of the finished bitmaps), then the in-superblock scan.
+                             uint32_t lbeg, uint32_t nl, uint16_t *__restrict__ rank_block,
+                             uint64_t *__restrict__ suptot, const uint32_t *err) {
+  // One warp per (level, superblock) of levels [lbeg, lbeg+nl): popcount of its
+  // <= 128 blocks of 8 words (a streaming read of the finished bitmaps), then
+  // the in-superblock scan.
   if (*err) return;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (gw >= (uint64_t)L * nsup_data) return;
-  const uint32_t l = (uint32_t)(gw / nsup_data);
+  if (gw >= (uint64_t)nl * nsup_data) return;
+  const uint32_t l = lbeg + (uint32_t)(gw / nsup_data);
   const uint64_t s = gw % nsup_data;
   const uint64_t b0 = s * 128;
   const uint64_t *B = bits + (uint64_t)l * wpl;
