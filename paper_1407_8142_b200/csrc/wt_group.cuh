@@ -94,20 +94,23 @@ constexpr int J0 = 2;   // levels split by the whole CTA (log2 WPB)
 // tile width (positions per tile): WT_GTT * 2 bytes of records per buffer
 template <typename RecT>
 struct GroupTile {
-  static constexpr int TT = sizeof(RecT) == 1 ? 2 * WT_GTT : (sizeof(RecT) == 2 ? WT_GTT : WT_GTT / 2);
-  static_assert(TT % (WPB * 256) == 0, "quarters are whole batches of 8 chunks");
+  static constexpr int TT = sizeof(RecT) == 1 ? 2 * WT_GTT : (sizeof(RecT) == 2 ? WT_GTT : (WT_GTT / 2) / 1024 * 1024);
+  static_assert(TT % (WPB * 256) == 0, "quarters are whole batches");
 };
 
 constexpr uint8_t CF_VALID = 1, CF_SHARED = 2;
 constexpr int TRASH = NDIG + 2;  // histogram bin of the load cover's out-of-tile records
 constexpr uint16_t FB_NONE = 0xffffu;
-constexpr int U = 8;  // chunks per software-pipelined batch
+#ifndef WT_U
+#define WT_U 8
+#endif
+constexpr int U = WT_U;  // chunks per software-pipelined batch
 
 template <typename RecT, bool HAS_OUT>
 struct GroupSmem {
   static constexpr int TT = GroupTile<RecT>::TT;
   static constexpr int NLB = TT / 32 + 8 * WPB;
-  static constexpr int NFB = TT / 256 + 2 * WPB;
+  static constexpr int NFB = TT / 128 + 2 * WPB;  // batches of >= 4 chunks
   alignas(16) RecT buf[2][TT + 16 / sizeof(RecT)];  // records, ping-pong between levels (+ load head)
   alignas(16) uint32_t H[NDIG + 4];        // tile digit counts, then their exclusive scan (H[ndig] = len)
   alignas(16) uint32_t BX[NDIG + 4];       // exclusive prefix over digits of same-row elements ahead of the tile
@@ -295,8 +298,8 @@ __device__ __forceinline__ uint32_t split_range(const uint16_t *T, const uint16_
       }
     }
     if (STORE_LB && lane == 0) {
-      sts_v4(LA + b * (4 * U), m[0], m[1], m[2], m[3]);
-      sts_v4(LA + b * (4 * U) + 16, m[4], m[5], m[6], m[7]);
+#pragma unroll
+      for (int u = 0; u < U; u += 4) sts_v4(LA + b * (4 * U) + 4 * u, m[u], m[u + 1], m[u + 2], m[u + 3]);
     }
   }
   const uint32_t nch = (wl + 31) >> 5;
@@ -537,7 +540,7 @@ __global__ void __launch_bounds__(WPB * 32, WT_GMINB) k_group(GroupParams p) {
         const uint32_t srcA = smem_u32(s.buf[k & 1]) + (k == 0 ? head0 * RB : 0u);
         const uint32_t dstA = smem_u32(s.buf[(k + 1) & 1]);
         uint32_t *LBq = s.LB + qlo / 32;
-        uint16_t *FBq = s.FB + warp * (QL / 256);
+        uint16_t *FBq = s.FB + warp * (QL / (32 * U));
         if (k > 0) {  // ones of the quarter at this level: a ballot pass (also the level's bitmap words)
           const uint32_t ones =
               split_range<RecT, false, true>(s.T, FBq, LBq, srcA, qlo, qhi - qlo, 0, bitsh, lane, lt);
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(WPB * 32, WT_GMINB) k_group(GroupParams p) {
         for (int w = 0; w < warp; w++) {
           const uint32_t l = s.H[(uint32_t)(w + 1) << shJ] - s.H[(uint32_t)w << shJ];
           lbo += ((l + 127) / 128) * 4;  // 16-byte aligned slices
-          fbo += l / 256;
+          fbo += l / (32 * U);
         }
         uint32_t *LBw = s.LB + lbo;
         uint16_t *FBw = s.FB + fbo;

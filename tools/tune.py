@@ -8,10 +8,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
-    "minb4_tt8k": ["WT_GMINB=4", "WT_GTT=8192"],
-    "minb5_tt8k": ["WT_GMINB=5", "WT_GTT=8192"],
-    "minb4_tt10k": ["WT_GMINB=4", "WT_GTT=10240"],
-    "minb3_tt12k": ["WT_GMINB=3", "WT_GTT=12288"],
+    "base": ["WT_GMINB=5", "WT_GTT=8192"],
+    "minb6_tt7k": ["WT_GMINB=6", "WT_GTT=7168"],
+    "u4_minb6_tt7k": ["WT_GMINB=6", "WT_GTT=7168", "WT_U=4"],
+    "u4": ["WT_GMINB=5", "WT_GTT=8192", "WT_U=4"],
 }
 CPW = os.environ.get("TUNE_CPW", "3").split(",")
 if sys.argv[1] == "build":
