@@ -48,6 +48,22 @@ class _Tree(ctypes.Structure):
     ]
 
 
+class _WM(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint64),
+        ("sigma", ctypes.c_uint64),
+        ("levels", ctypes.c_uint32),
+        ("elem_bytes", ctypes.c_uint32),
+        ("words_per_level", ctypes.c_uint64),
+        ("bits", ctypes.POINTER(ctypes.c_uint64)),
+        ("zeros", ctypes.POINTER(ctypes.c_uint64)),
+        ("blocks_per_level", ctypes.c_uint64),
+        ("supers_per_level", ctypes.c_uint64),
+        ("rank_block", ctypes.POINTER(ctypes.c_uint16)),
+        ("rank_super", ctypes.POINTER(ctypes.c_uint64)),
+    ]
+
+
 def compile_oracle(force: bool = False) -> str:
     """Compile wt_oracle.c with gcc into oracle/liboracle.so (idempotent)."""
     if (not force and os.path.exists(_LIB)
@@ -78,6 +94,15 @@ def _load():
             lib.oracle_rank1.restype = ctypes.c_uint64
             lib.oracle_levels.argtypes = [ctypes.c_uint64]
             lib.oracle_levels.restype = ctypes.c_uint32
+            lib.oracle_wm_build.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
+                                            ctypes.c_uint64, ctypes.POINTER(ctypes.POINTER(_WM))]
+            lib.oracle_wm_build.restype = ctypes.c_int
+            lib.oracle_wm_free.argtypes = [ctypes.POINTER(_WM)]
+            lib.oracle_wm_free.restype = None
+            lib.oracle_wm_access.argtypes = [ctypes.POINTER(_WM), ctypes.c_uint64]
+            lib.oracle_wm_access.restype = ctypes.c_uint32
+            lib.oracle_wm_rank.argtypes = [ctypes.POINTER(_WM), ctypes.c_uint32, ctypes.c_uint64]
+            lib.oracle_wm_rank.restype = ctypes.c_uint64
             _lib = lib
     return _lib
 
@@ -173,3 +198,65 @@ def build(seq: np.ndarray, sigma: int) -> dict:
 
 def levels(sigma: int) -> int:
     return int(_load().oracle_levels(int(sigma)))
+
+
+class OracleWM:
+    """Owns one C oracle wavelet matrix; arrays copied out."""
+
+    def __init__(self, seq: np.ndarray, sigma: int):
+        lib = _load()
+        seq = np.ascontiguousarray(seq)
+        if seq.dtype not in (np.uint8, np.uint16, np.uint32):
+            raise TypeError("seq must be uint8/uint16/uint32")
+        out = ctypes.POINTER(_WM)()
+        rc = lib.oracle_wm_build(seq.ctypes.data if seq.size else None, seq.size,
+                                 seq.dtype.itemsize, int(sigma), ctypes.byref(out))
+        if rc != OK:
+            raise OracleError(rc)
+        self._lib = lib
+        self._m = out
+        m = out.contents
+        self.n, self.sigma, self.levels = m.n, m.sigma, m.levels
+        self.words_per_level = m.words_per_level
+        self.blocks_per_level = m.blocks_per_level
+        self.supers_per_level = m.supers_per_level
+
+    def arrays(self) -> dict:
+        m = self._m.contents
+        L = m.levels
+        return {
+            "bits": _copy(m.bits, L * m.words_per_level, np.uint64),
+            "zeros": _copy(m.zeros, L, np.uint64),
+            "rank_block": _copy(m.rank_block, L * m.blocks_per_level, np.uint16),
+            "rank_super": _copy(m.rank_super, L * m.supers_per_level, np.uint64),
+        }
+
+    def access(self, positions) -> np.ndarray:
+        return np.array([self._lib.oracle_wm_access(self._m, int(i)) for i in positions], dtype=np.uint32)
+
+    def rank(self, symbols, positions) -> np.ndarray:
+        return np.array([self._lib.oracle_wm_rank(self._m, int(c), int(i))
+                         for c, i in zip(symbols, positions)], dtype=np.uint64)
+
+    def close(self):
+        if getattr(self, "_m", None):
+            self._lib.oracle_wm_free(self._m)
+            self._m = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def wm_build(seq: np.ndarray, sigma: int) -> dict:
+    """Oracle wavelet matrix; returns bits, zeros, rank_block, rank_super (+ metadata)."""
+    with OracleWM(seq, sigma) as m:
+        out = m.arrays()
+        out.update(n=m.n, sigma=m.sigma, levels=m.levels, words_per_level=m.words_per_level,
+                   blocks_per_level=m.blocks_per_level, supers_per_level=m.supers_per_level)
+    return out

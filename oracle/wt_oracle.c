@@ -137,6 +137,26 @@ static uint32_t bitlen_minus1(uint64_t sigma) {
 
 static uint32_t popcount64(uint64_t w) { return (uint32_t)__builtin_popcountll(w); }
 
+/* rank directory (:805-814 with reading R-9): walk the 512-bit blocks of each
+ * level; block entries count the ones before the block inside its
+ * superblock, superblock entries the ones before the superblock, and the
+ * last superblock entry is the level total. */
+static void rank_directory(const uint64_t *bits, uint32_t L, uint64_t wpl, uint64_t bpl, uint64_t spl,
+                           uint16_t *rank_block, uint64_t *rank_super) {
+  for (uint32_t l = 0; l < L; l++) {
+    const uint64_t *B = bits + (uint64_t)l * wpl;
+    uint16_t *blk = rank_block + (uint64_t)l * bpl;
+    uint64_t *sup = rank_super + (uint64_t)l * spl;
+    uint64_t ones = 0, base = 0;
+    for (uint64_t k = 0; k < bpl; k++) {
+      if (k % 128 == 0) { sup[k / 128] = ones; base = ones; }
+      blk[k] = (uint16_t)(ones - base);
+      for (int w = 0; w < 8; w++) ones += popcount64(B[k * 8 + w]);
+    }
+    sup[spl - 1] = ones; /* the level total */
+  }
+}
+
 void oracle_free(oracle_tree *t) {
   if (!t) return;
   free(t->bits);
@@ -240,19 +260,8 @@ int oracle_build(const void *seq, uint64_t n, uint32_t elem_bytes, uint64_t sigm
   }
   free(b.nodes);
 
-  /* rank directory (:805-814 with reading R-9): walk the 512-bit blocks */
-  for (uint32_t l = 0; l < L; l++) {
-    const uint64_t *B = t->bits + (uint64_t)l * t->words_per_level;
-    uint16_t *blk = t->rank_block + (uint64_t)l * t->blocks_per_level;
-    uint64_t *sup = t->rank_super + (uint64_t)l * t->supers_per_level;
-    uint64_t ones = 0, base = 0;
-    for (uint64_t k = 0; k < t->blocks_per_level; k++) {
-      if (k % 128 == 0) { sup[k / 128] = ones; base = ones; }
-      blk[k] = (uint16_t)(ones - base);
-      for (int w = 0; w < 8; w++) ones += popcount64(B[k * 8 + w]);
-    }
-    sup[t->supers_per_level - 1] = ones; /* the level total */
-  }
+  rank_directory(t->bits, L, t->words_per_level, t->blocks_per_level, t->supers_per_level, t->rank_block,
+                 t->rank_super);
   *out = t;
   return OR_OK;
 }
@@ -314,4 +323,155 @@ uint64_t oracle_rank(const oracle_tree *t, uint32_t c, uint64_t i) {
     if (r == 0) return 0;
   }
   return r;
+}
+
+
+/* ======================================================================
+ * Wavelet matrix (§7 "Extensions").
+ *
+ *   "on level l, all symbols with a 0 as their l'th highest bit are
+ *    represented on the left side of the level's bitmap and all symbols
+ *    with a 1 ... on the right.  Each level stores the number of 0's on the
+ *    level.  The bitmap is filled based on the l+1'st highest bit" (:911-916)
+ *   "we proceed level-by-level and stably reorder S based on the l'th
+ *    highest bit of the symbols using ... prefix sum (similar to levelWT)
+ *    ... which also gives the number of 0's on the level" (:917-921)
+ *
+ * So: A_0 = S; level l's bitmap holds bit (L-1-l) of A_l[i] (the (l+1)'st
+ * highest); zeros[l] = number of 0 bits of level l; A_{l+1} = A_l stably
+ * reordered by that bit, zeros first, with the prefix sum of levelWT's
+ * Fig. 1 l.12-17 over the whole level (one node).  Same bit layout and rank
+ * directory as the tree above.
+ * ====================================================================== */
+typedef struct {
+  uint64_t n;
+  uint64_t sigma;
+  uint32_t levels;
+  uint32_t elem_bytes;
+  uint64_t words_per_level;
+  uint64_t *bits;            /* levels * words_per_level, LSB-first      */
+  uint64_t *zeros;           /* levels: number of 0 bits of each level   */
+  uint64_t blocks_per_level;
+  uint64_t supers_per_level;
+  uint16_t *rank_block;
+  uint64_t *rank_super;
+} oracle_wm;
+
+void oracle_wm_free(oracle_wm *m) {
+  if (!m) return;
+  free(m->bits);
+  free(m->zeros);
+  free(m->rank_block);
+  free(m->rank_super);
+  free(m);
+}
+
+int oracle_wm_build(const void *seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma, oracle_wm **out) {
+  if (!out) return OR_EINVAL;
+  *out = NULL;
+  if ((n > 0 && !seq) || (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4))
+    return OR_EINVAL;
+  if (sigma < 1 || sigma > ((uint64_t)1 << (8 * elem_bytes)) || n >= ((uint64_t)1 << 32))
+    return OR_EINVAL;
+  uint32_t L = bitlen_minus1(sigma);
+  uint32_t *A = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint32_t *T = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint32_t *X = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+  if (!A || !T || !X) { free(A); free(T); free(X); return OR_ENOMEM; }
+  for (uint64_t i = 0; i < n; i++) {
+    uint32_t v;
+    if (elem_bytes == 1) v = ((const uint8_t *)seq)[i];
+    else if (elem_bytes == 2) v = ((const uint16_t *)seq)[i];
+    else v = ((const uint32_t *)seq)[i];
+    if ((uint64_t)v >= sigma) { free(A); free(T); free(X); return OR_ESYMBOL; }
+    A[i] = v;
+  }
+  oracle_wm *m = (oracle_wm *)calloc(1, sizeof(oracle_wm));
+  if (!m) { free(A); free(T); free(X); return OR_ENOMEM; }
+  m->n = n;
+  m->sigma = sigma;
+  m->levels = L;
+  m->elem_bytes = elem_bytes;
+  m->words_per_level = ((n + 511) / 512) * 8;
+  m->blocks_per_level = (n + 511) / 512;
+  m->supers_per_level = (n + 65535) / 65536 + 1;
+  uint64_t nbits = (uint64_t)L * m->words_per_level;
+  m->bits = (uint64_t *)calloc(nbits ? nbits : 1, sizeof(uint64_t));
+  m->zeros = (uint64_t *)calloc(L ? L : 1, sizeof(uint64_t));
+  m->rank_block = (uint16_t *)calloc(L * m->blocks_per_level + 1, sizeof(uint16_t));
+  m->rank_super = (uint64_t *)calloc(L * m->supers_per_level + 1, sizeof(uint64_t));
+  if (!m->bits || !m->zeros || !m->rank_block || !m->rank_super) {
+    free(A); free(T); free(X); oracle_wm_free(m);
+    return OR_ENOMEM;
+  }
+  for (uint32_t l = 0; l < L; l++) {
+    uint32_t shift = L - (l + 1); /* the (l+1)'st highest bit (:915-916) */
+    uint64_t *B = m->bits + (uint64_t)l * m->words_per_level;
+    /* X[i] = 1 for a 0 bit; exclusive prefix sum X, total X_s = zeros (Fig. 1 l.12-14) */
+    uint64_t Xs = 0;
+    for (uint64_t i = 0; i < n; i++) {
+      X[i] = (uint32_t)Xs;
+      Xs += ((A[i] >> shift) & 1u) == 0;
+    }
+    m->zeros[l] = Xs;
+    /* fill the bitmap and reorder stably, zeros first (Fig. 1 l.15-17, one node) */
+    for (uint64_t i = 0; i < n; i++) {
+      if ((A[i] >> shift) & 1u) {
+        B[i >> 6] |= (uint64_t)1 << (i & 63);
+        T[Xs + i - X[i]] = A[i];
+      } else {
+        T[X[i]] = A[i];
+      }
+    }
+    uint32_t *tmp = A; A = T; T = tmp; /* swap(S, S') */
+  }
+  free(A); free(T); free(X);
+  rank_directory(m->bits, L, m->words_per_level, m->blocks_per_level, m->supers_per_level, m->rank_block,
+                 m->rank_super);
+  *out = m;
+  return OR_OK;
+}
+
+static uint64_t wm_rank1(const oracle_wm *m, uint32_t l, uint64_t i) {
+  if (i >= m->n) return m->rank_super[(uint64_t)l * m->supers_per_level + m->supers_per_level - 1];
+  const uint64_t *B = m->bits + (uint64_t)l * m->words_per_level;
+  uint64_t r = m->rank_super[(uint64_t)l * m->supers_per_level + (i >> 16)];
+  r += m->rank_block[(uint64_t)l * m->blocks_per_level + (i >> 9)];
+  for (uint64_t w = (i >> 9) * 8; w < (i >> 6); w++) r += popcount64(B[w]);
+  if (i & 63) r += popcount64(B[i >> 6] & (((uint64_t)1 << (i & 63)) - 1));
+  return r;
+}
+
+/* access(i): the bit at i selects the side; a 0 moves to rank0(i), a 1 to
+ * zeros[l] + rank1(i) (the reorder of :917-921 applied to one position) */
+uint32_t oracle_wm_access(const oracle_wm *m, uint64_t i) {
+  if (!m || i >= m->n) return UINT32_MAX;
+  uint32_t sym = 0;
+  for (uint32_t l = 0; l < m->levels; l++) {
+    const uint64_t *B = m->bits + (uint64_t)l * m->words_per_level;
+    uint32_t bit = (uint32_t)((B[i >> 6] >> (i & 63)) & 1u);
+    uint64_t r1 = wm_rank1(m, l, i);
+    sym = (sym << 1) | bit;
+    i = bit ? m->zeros[l] + r1 : i - r1;
+  }
+  return sym;
+}
+
+/* rank_c(i), inclusive (:205-206): track the range [s, e) of the positions
+ * 0..i that share c's leading bits, level by level */
+uint64_t oracle_wm_rank(const oracle_wm *m, uint32_t c, uint64_t i) {
+  if (!m || i >= m->n || (uint64_t)c >= m->sigma) return UINT64_MAX;
+  uint64_t s = 0, e = i + 1;
+  for (uint32_t l = 0; l < m->levels; l++) {
+    uint64_t r1s = wm_rank1(m, l, s), r1e = wm_rank1(m, l, e);
+    if ((c >> (m->levels - 1 - l)) & 1u) {
+      s = m->zeros[l] + r1s;
+      e = m->zeros[l] + r1e;
+    } else {
+      s = s - r1s;
+      e = e - r1e;
+    }
+    if (s == e) return 0;
+  }
+  return e - s;
 }

@@ -128,3 +128,37 @@ def nodes_from_csr(arrs) -> list:
         lo, hi = int(ptr[l]), int(ptr[l + 1])
         out.append(list(zip(arrs["node_key"][lo:hi].tolist(), arrs["node_start"][lo:hi].tolist())))
     return out
+
+
+def wm_sort(S: np.ndarray, sigma: int):
+    """Wavelet matrix by its sort characterisation ("a strategy
+    similar to sortWT, but using the reverse of the top l bits as the key when
+    sorting"): level l's sequence is S stably sorted by the bit-reversed top l
+    bits; its bitmap holds bit L-1-l; zeros[l] counts its 0 bits.
+    Returns (bits [L*WPL] u64, zeros [L] u64)."""
+    S = np.asarray(S).astype(np.uint64)
+    n = S.size
+    L = levels_of(sigma)
+    W = wpl(n)
+    bits = np.zeros(L * W, dtype=np.uint64)
+    zeros = np.zeros(L, dtype=np.uint64)
+    for l in range(L):
+        top = S >> np.uint64(L - l) if l else np.zeros(n, dtype=np.uint64)
+        key = np.zeros(n, dtype=np.uint64)
+        for j in range(l):  # reverse the l-bit prefix
+            key |= ((top >> np.uint64(j)) & np.uint64(1)) << np.uint64(l - 1 - j)
+        order = np.argsort(key, kind="stable")
+        Sl = S[order]
+        b = ((Sl >> np.uint64(L - 1 - l)) & np.uint64(1)).astype(np.uint8)
+        bits[l * W:(l + 1) * W] = pack_bits(b, W)
+        zeros[l] = n - int(b.sum())
+    return bits, zeros
+
+
+def wm_access_rank_bruteforce(S: np.ndarray):
+    """access(i) = S[i]; rank_c(i) = #{j <= i : S[j] = c}."""
+    S = np.asarray(S)
+
+    def rank(c, i):
+        return int(np.count_nonzero(S[:i + 1] == c))
+    return (lambda i: int(S[i])), rank
