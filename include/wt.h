@@ -125,6 +125,45 @@ int wt_access(const wt_tree *t, const uint64_t *d_pos, uint64_t q, uint32_t *d_o
 int wt_rank(const wt_tree *t, const uint32_t *d_sym, const uint64_t *d_pos, uint64_t q,
             uint64_t *d_out, void *stream);
 
+/* ---- wavelet matrix ----
+ *
+ * Level l's bitmap holds the (l+1)'st highest bit of A_l, where A_0 = S and
+ * A_{l+1} is A_l stably reordered by level l's bit, zeros first (:911-921);
+ * equivalently A_l is S stably sorted by the reverse of its top l bits
+ * (:924-925).  Each level stores its number of 0 bits (:914).  Bits, padding
+ * and rank directory use exactly the layout of wt_tree above; there is no
+ * node table (a level is one sequence).
+ */
+typedef struct wm_matrix {
+  uint64_t n;                 /* sequence length                              */
+  uint64_t sigma;             /* alphabet size                                */
+  uint32_t levels;            /* L = ceil(log2 sigma)                         */
+  uint32_t elem_bytes;        /* bytes per input symbol                       */
+  uint64_t words_per_level;   /* ceil(n/512) * 8                              */
+  uint64_t *bits;             /* u64[levels * words_per_level] (device)       */
+  uint64_t *zeros;            /* u64[levels]: 0 bits of each level (device)   */
+  uint64_t blocks_per_level;  /* ceil(n/512)                                  */
+  uint64_t supers_per_level;  /* ceil(n/65536) + 1                            */
+  uint16_t *rank_block;       /* u16[levels * blocks_per_level] (device)      */
+  uint64_t *rank_super;       /* u64[levels * supers_per_level] (device)      */
+  void *internal;             /* library bookkeeping; do not touch            */
+} wm_matrix;
+
+/* wm_build -- build the wavelet matrix of S.  Arguments, stream semantics,
+ * ownership and errors exactly as wt_build (WT_ESYMBOL for S[i] >= sigma,
+ * WT_EINVAL for bad arguments, one stream synchronisation at the end). */
+int wm_build(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma,
+             void *stream, wm_matrix **out);
+/* wm_free -- release everything owned by m; NULL is a no-op. */
+int wm_free(wm_matrix *m);
+/* wm_access / wm_rank -- batched access(S, i) and inclusive rank_c(S, i)
+ * on the matrix: a 0 bit at level l maps i to rank0(i),
+ * a 1 bit to zeros[l] + rank1(i).  Buffers, sentinels and errors exactly as
+ * wt_access / wt_rank. */
+int wm_access(const wm_matrix *m, const uint64_t *d_pos, uint64_t q, uint32_t *d_out, void *stream);
+int wm_rank(const wm_matrix *m, const uint32_t *d_sym, const uint64_t *d_pos, uint64_t q,
+            uint64_t *d_out, void *stream);
+
 /* ---- measurement hooks (used by bench.py; no effect on results) ---- */
 
 #define WT_PROF_MAX 32

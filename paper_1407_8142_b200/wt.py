@@ -59,6 +59,23 @@ def lib_path() -> str:
     return _LIB_PATH
 
 
+class _WmMatrix(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint64),
+        ("sigma", ctypes.c_uint64),
+        ("levels", ctypes.c_uint32),
+        ("elem_bytes", ctypes.c_uint32),
+        ("words_per_level", ctypes.c_uint64),
+        ("bits", ctypes.c_void_p),
+        ("zeros", ctypes.c_void_p),
+        ("blocks_per_level", ctypes.c_uint64),
+        ("supers_per_level", ctypes.c_uint64),
+        ("rank_block", ctypes.c_void_p),
+        ("rank_super", ctypes.c_void_p),
+        ("internal", ctypes.c_void_p),
+    ]
+
+
 def _load():
     global _lib
     if _lib is not None:
@@ -86,6 +103,17 @@ def _load():
     lib.wt_last_profile.restype = ctypes.c_int
     lib.wt_version.argtypes = []
     lib.wt_version.restype = ctypes.c_char_p
+    PM = ctypes.POINTER(_WmMatrix)
+    lib.wm_build.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                             ctypes.c_void_p, ctypes.POINTER(PM)]
+    lib.wm_build.restype = ctypes.c_int
+    lib.wm_free.argtypes = [PM]
+    lib.wm_free.restype = ctypes.c_int
+    lib.wm_access.argtypes = [PM, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+    lib.wm_access.restype = ctypes.c_int
+    lib.wm_rank.argtypes = [PM, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                            ctypes.c_void_p]
+    lib.wm_rank.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -267,3 +295,91 @@ def last_profile() -> dict:
 
 def version() -> str:
     return _load().wt_version().decode()
+
+
+
+# ---------------------------------------------------------------- wavelet matrix
+class WaveletMatrix:
+    """A built wavelet matrix (PAPER.md:910-925).  Arrays are zero-copy torch
+    views of library memory, valid until ``free()``."""
+
+    def __init__(self, handle, device):
+        self._h = handle
+        m = handle.contents
+        self.device = device
+        self.n, self.sigma, self.levels = int(m.n), int(m.sigma), int(m.levels)
+        self.words_per_level = int(m.words_per_level)
+        self.blocks_per_level = int(m.blocks_per_level)
+        self.supers_per_level = int(m.supers_per_level)
+        L = self.levels
+        self.bits = _view(m.bits, L * self.words_per_level, "<u8", torch.uint64, device)
+        self.zeros = _view(m.zeros, L, "<u8", torch.uint64, device)
+        self.rank_block = _view(m.rank_block, L * self.blocks_per_level, "<u2", torch.uint16, device)
+        self.rank_super = _view(m.rank_super, L * self.supers_per_level, "<u8", torch.uint64, device)
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("matrix already freed")
+        return self._h
+
+    def numpy(self) -> dict:
+        out = {k: getattr(self, k).cpu().numpy() for k in ("bits", "zeros", "rank_block", "rank_super")}
+        out.update(n=self.n, sigma=self.sigma, levels=self.levels, words_per_level=self.words_per_level,
+                   blocks_per_level=self.blocks_per_level, supers_per_level=self.supers_per_level)
+        return out
+
+    def access(self, pos: torch.Tensor, stream=None) -> torch.Tensor:
+        lib = _load()
+        pos = pos.contiguous().view(-1)
+        out = torch.empty(pos.numel(), dtype=torch.int32, device=pos.device)
+        rc = lib.wm_access(self.handle, ctypes.c_void_p(pos.data_ptr() if pos.numel() else 0), pos.numel(),
+                           ctypes.c_void_p(out.data_ptr() if out.numel() else 0),
+                           ctypes.c_void_p(_stream_ptr(stream)))
+        if rc != WT_OK:
+            raise WtError(rc, "wm_access")
+        return out.view(torch.uint32)
+
+    def rank(self, sym: torch.Tensor, pos: torch.Tensor, stream=None) -> torch.Tensor:
+        lib = _load()
+        sym = sym.contiguous().view(-1)
+        pos = pos.contiguous().view(-1)
+        if sym.numel() != pos.numel():
+            raise ValueError("sym and pos must have the same length")
+        out = torch.empty(pos.numel(), dtype=torch.int64, device=pos.device)
+        rc = lib.wm_rank(self.handle, ctypes.c_void_p(sym.data_ptr() if sym.numel() else 0),
+                         ctypes.c_void_p(pos.data_ptr() if pos.numel() else 0), pos.numel(),
+                         ctypes.c_void_p(out.data_ptr() if out.numel() else 0),
+                         ctypes.c_void_p(_stream_ptr(stream)))
+        if rc != WT_OK:
+            raise WtError(rc, "wm_rank")
+        return out.view(torch.uint64)
+
+    def free(self):
+        if self._h is not None:
+            for k in ("bits", "zeros", "rank_block", "rank_super"):
+                setattr(self, k, None)
+            rc = _load().wm_free(self._h)
+            self._h = None
+            if rc != WT_OK:
+                raise WtError(rc, "wm_free")
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def wm_build(seq: torch.Tensor, sigma: int, stream=None) -> WaveletMatrix:
+    """wm_build on a CUDA tensor holding S (8/16/32-bit integers, read as unsigned)."""
+    lib = _load()
+    if not seq.is_cuda:
+        raise ValueError("wm_build() needs a CUDA tensor")
+    seq = seq.contiguous().view(-1)
+    out = ctypes.POINTER(_WmMatrix)()
+    rc = lib.wm_build(ctypes.c_void_p(seq.data_ptr() if seq.numel() else 0), seq.numel(),
+                      _elem_bytes(seq), int(sigma), ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out))
+    if rc != WT_OK:
+        raise WtError(rc, "wm_build")
+    return WaveletMatrix(out, seq.device)

@@ -14,12 +14,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "wt.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(wt_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(w[tm]_\w+)\s*\(", src, flags=re.M)))
 
 
 def test_header_declares_expected_calls():
     names = _declared()
-    for req in ("wt_build", "wt_build_host", "wt_free", "wt_access", "wt_rank"):
+    for req in ("wt_build", "wt_build_host", "wt_free", "wt_access", "wt_rank",
+                "wm_build", "wm_free", "wm_access", "wm_rank"):
         assert req in names
 
 
@@ -48,6 +49,10 @@ def test_null_and_argument_errors_without_gpu():
     lib = wt._load()
     out = ctypes.POINTER(wt._WtTree)()
     assert lib.wt_build(None, 10, 1, 4, None, ctypes.byref(out)) == wt.WT_EINVAL
+    mout = ctypes.POINTER(wt._WmMatrix)()
+    assert lib.wm_build(None, 10, 1, 4, None, ctypes.byref(mout)) == wt.WT_EINVAL
+    assert lib.wm_build(None, 0, 3, 4, None, ctypes.byref(mout)) == wt.WT_EINVAL
+    assert lib.wm_free(None) == wt.WT_OK
     assert lib.wt_build(ctypes.c_void_p(16), 10, 3, 4, None, ctypes.byref(out)) == wt.WT_EINVAL
     assert lib.wt_build(ctypes.c_void_p(16), 10, 1, 257, None, ctypes.byref(out)) == wt.WT_EINVAL
     assert lib.wt_build(ctypes.c_void_p(16), 10, 1, 0, None, ctypes.byref(out)) == wt.WT_EINVAL

@@ -9,9 +9,6 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
     "base": ["WT_GMINB=5", "WT_GTT=8192"],
-    "minb6_tt7k": ["WT_GMINB=6", "WT_GTT=7168"],
-    "u4_minb6_tt7k": ["WT_GMINB=6", "WT_GTT=7168", "WT_U=4"],
-    "u4": ["WT_GMINB=5", "WT_GTT=8192", "WT_U=4"],
 }
 CPW = os.environ.get("TUNE_CPW", "3").split(",")
 if sys.argv[1] == "build":
