@@ -104,6 +104,18 @@ constexpr uint16_t FB_NONE = 0xffffu;
 #ifndef WT_U
 #define WT_U 8
 #endif
+// running ones count of a chunk: WT_CNT_REDUX=1 uses the warp reduction (a
+// uniform result, off the MIO pipe that POPC shares with shared memory)
+#ifndef WT_CNT_REDUX
+#define WT_CNT_REDUX 0
+#endif
+__device__ __forceinline__ uint32_t chunk_ones(uint32_t m, bool P) {
+#if WT_CNT_REDUX
+  return __reduce_add_sync(0xffffffffu, P ? 1u : 0u);
+#else
+  return __popc(m);
+#endif
+}
 constexpr int U = WT_U;  // chunks per software-pipelined batch
 
 template <typename RecT, bool HAS_OUT>
@@ -274,7 +286,7 @@ __device__ __forceinline__ uint32_t split_range(const uint16_t *T, const uint16_
           const uint32_t O = Orun + __popc(m[u] & lt);
           const uint32_t Z = pb + u * 32 - O;
           sts<RecT>(P ? a1 + RB * O : a0 + RB * Z, r[u]);
-          Orun += __popc(m[u]);
+          Orun += chunk_ones(m[u], P);
         }
       } else {
         uint32_t t[U];
@@ -287,7 +299,7 @@ __device__ __forceinline__ uint32_t split_range(const uint16_t *T, const uint16_
           const uint32_t O = Orun + __popc(m[u] & lt);
           const uint32_t Z = pb + u * 32 - O;
           sts<RecT>(t[u] + RB * (P ? O : Z), r[u]);
-          Orun += __popc(m[u]);
+          Orun += chunk_ones(m[u], P);
         }
       }
     } else {

@@ -9,6 +9,7 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
     "base": ["WT_GMINB=5", "WT_GTT=8192"],
+    "redux": ["WT_GMINB=5", "WT_GTT=8192", "WT_CNT_REDUX=1"],
 }
 CPW = os.environ.get("TUNE_CPW", "3").split(",")
 if sys.argv[1] == "build":
