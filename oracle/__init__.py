@@ -103,6 +103,20 @@ def _load():
             lib.oracle_wm_access.restype = ctypes.c_uint32
             lib.oracle_wm_rank.argtypes = [ctypes.POINTER(_WM), ctypes.c_uint32, ctypes.c_uint64]
             lib.oracle_wm_rank.restype = ctypes.c_uint64
+            PU = ctypes.POINTER(ctypes.POINTER(ctypes.c_uint32))
+            lib.oracle_select_dir.argtypes = [ctypes.POINTER(_Tree), PU, PU, ctypes.POINTER(ctypes.c_uint64)]
+            lib.oracle_select_dir.restype = ctypes.c_int
+            lib.oracle_wm_select_dir.argtypes = [ctypes.POINTER(_WM), PU, PU, ctypes.POINTER(ctypes.c_uint64)]
+            lib.oracle_wm_select_dir.restype = ctypes.c_int
+            lib.oracle_free_buf.argtypes = [ctypes.c_void_p]
+            lib.oracle_free_buf.restype = None
+            U32P = ctypes.POINTER(ctypes.c_uint32)
+            lib.oracle_select.argtypes = [ctypes.POINTER(_Tree), U32P, U32P, ctypes.c_uint64, ctypes.c_uint32,
+                                          ctypes.c_uint64]
+            lib.oracle_select.restype = ctypes.c_uint64
+            lib.oracle_wm_select.argtypes = [ctypes.POINTER(_WM), U32P, U32P, ctypes.c_uint64, ctypes.c_uint32,
+                                             ctypes.c_uint64]
+            lib.oracle_wm_select.restype = ctypes.c_uint64
             _lib = lib
     return _lib
 
@@ -119,7 +133,47 @@ def _copy(ptr, count, dtype):
     return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True)
 
 
-class OracleTree:
+
+
+def _select_dir(lib, fn, handle, levels):
+    """Run a select-directory builder; returns (sel0, sel1, sps, raw pointers)."""
+    s0 = ctypes.POINTER(ctypes.c_uint32)()
+    s1 = ctypes.POINTER(ctypes.c_uint32)()
+    sps = ctypes.c_uint64()
+    rc = fn(handle, ctypes.byref(s0), ctypes.byref(s1), ctypes.byref(sps))
+    if rc != OK:
+        raise OracleError(rc)
+    cnt = levels * sps.value
+    a0, a1 = _copy(s0, cnt, np.uint32), _copy(s1, cnt, np.uint32)
+    return a0, a1, sps.value, (s0, s1)
+
+
+class _SelectMixin:
+    """select_c and the sampled select directory."""
+
+    def _sel(self):
+        if getattr(self, "_seldir", None) is None:
+            self._seldir = _select_dir(self._lib, self._sel_dir_fn, self._handle(), self.levels)
+        return self._seldir
+
+    def select_dir(self) -> dict:
+        a0, a1, sps, _ = self._sel()
+        return {"select0": a0, "select1": a1, "select_per_level": sps}
+
+    def select(self, symbols, ks) -> np.ndarray:
+        _, _, sps, (p0, p1) = self._sel()
+        return np.array([self._sel_fn(self._handle(), p0, p1, sps, int(c), int(k))
+                         for c, k in zip(symbols, ks)], dtype=np.uint64)
+
+    def _free_sel(self):
+        sd = getattr(self, "_seldir", None)
+        if sd is not None:
+            self._lib.oracle_free_buf(sd[3][0])
+            self._lib.oracle_free_buf(sd[3][1])
+            self._seldir = None
+
+
+class OracleTree(_SelectMixin):
     """Owns one C oracle tree; arrays are copied out into numpy."""
 
     def __init__(self, seq: np.ndarray, sigma: int):
@@ -170,7 +224,12 @@ class OracleTree:
     def rank1(self, level: int, i: int) -> int:
         return int(self._lib.oracle_rank1(self._t, level, i))
 
+    _handle = property(lambda self: (lambda: self._t))
+    _sel_dir_fn = property(lambda self: self._lib.oracle_select_dir)
+    _sel_fn = property(lambda self: self._lib.oracle_select)
+
     def close(self):
+        self._free_sel()
         if getattr(self, "_t", None):
             self._lib.oracle_free(self._t)
             self._t = None
@@ -185,10 +244,13 @@ class OracleTree:
         self.close()
 
 
-def build(seq: np.ndarray, sigma: int) -> dict:
-    """Oracle construction; returns the §8(b) arrays plus scalar metadata."""
+def build(seq: np.ndarray, sigma: int, select: bool = False) -> dict:
+    """Oracle construction; returns the §8(b) arrays plus scalar metadata
+    (and the select directory when ``select``)."""
     with OracleTree(seq, sigma) as t:
         out = t.arrays()
+        if select:
+            out.update(t.select_dir())
         out.update(n=t.n, sigma=t.sigma, levels=t.levels,
                    words_per_level=t.words_per_level,
                    blocks_per_level=t.blocks_per_level,
@@ -200,7 +262,7 @@ def levels(sigma: int) -> int:
     return int(_load().oracle_levels(int(sigma)))
 
 
-class OracleWM:
+class OracleWM(_SelectMixin):
     """Owns one C oracle wavelet matrix; arrays copied out."""
 
     def __init__(self, seq: np.ndarray, sigma: int):
@@ -238,7 +300,12 @@ class OracleWM:
         return np.array([self._lib.oracle_wm_rank(self._m, int(c), int(i))
                          for c, i in zip(symbols, positions)], dtype=np.uint64)
 
+    _handle = property(lambda self: (lambda: self._m))
+    _sel_dir_fn = property(lambda self: self._lib.oracle_wm_select_dir)
+    _sel_fn = property(lambda self: self._lib.oracle_wm_select)
+
     def close(self):
+        self._free_sel()
         if getattr(self, "_m", None):
             self._lib.oracle_wm_free(self._m)
             self._m = None
@@ -257,6 +324,7 @@ def wm_build(seq: np.ndarray, sigma: int) -> dict:
     """Oracle wavelet matrix; returns bits, zeros, rank_block, rank_super (+ metadata)."""
     with OracleWM(seq, sigma) as m:
         out = m.arrays()
+        out.update(m.select_dir())
         out.update(n=m.n, sigma=m.sigma, levels=m.levels, words_per_level=m.words_per_level,
                    blocks_per_level=m.blocks_per_level, supers_per_level=m.supers_per_level)
     return out

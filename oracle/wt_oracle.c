@@ -475,3 +475,142 @@ uint64_t oracle_wm_rank(const oracle_wm *m, uint32_t c, uint64_t i) {
   }
   return e - s;
 }
+
+/* ======================================================================
+ * Select (§6 :827-845).
+ *
+ * select_c(S, k) = position of the k'th occurrence of c (k >= 1, 0-based
+ * positions; UINT64_MAX when k == 0, k > the count of c, or c >= sigma).
+ *
+ * Select directory (Clark's first level, :827-829, with DESIGN.md reading
+ * R-14 fixing the sampling): per level, the positions of all 1 bits (and of
+ * all 0 bits) are computed "using a prefix sum and filter" (:839-841) and
+ * every 4096'th is kept: sel1[l*SPS + j] = position of the (4096 j)'th 1 bit
+ * (0-based count), sel0 likewise for 0 bits; SPS = ceil(n / 4096) + 1 and
+ * entries past the last sample are n.
+ *
+ * select_b(l, k) on a level bitmap scans forward from the sample of the
+ * k'th b-bit; select_c descends top-down to find c's node (tree) or class
+ * start (matrix) at every level, then climbs back up with select_b.
+ * ====================================================================== */
+#define OR_SEL_SAMPLE 4096u
+
+static uint64_t sel_per_level(uint64_t n) { return (n + OR_SEL_SAMPLE - 1) / OR_SEL_SAMPLE + 1; }
+
+/* filter the positions of the b-bits of one level, keep every 4096'th */
+static void select_samples(const uint64_t *B, uint64_t n, uint32_t b, uint32_t *out, uint64_t sps) {
+  uint64_t cnt = 0, j = 0;
+  for (uint64_t i = 0; i < n; i++) {
+    uint32_t bit = (uint32_t)((B[i >> 6] >> (i & 63)) & 1u);
+    if (bit == b) {
+      if (cnt % OR_SEL_SAMPLE == 0) out[j++] = (uint32_t)i;
+      cnt++;
+    }
+  }
+  for (; j < sps; j++) out[j] = (uint32_t)n;
+}
+
+/* select_b(l, k): position of the k'th (1-based) b-bit of a level; n if none */
+static uint64_t level_select(const uint64_t *B, uint64_t n, const uint32_t *samples, uint32_t b, uint64_t k) {
+  if (k == 0) return n;
+  uint64_t j = (k - 1) / OR_SEL_SAMPLE;
+  uint64_t i = samples[j];
+  if (i >= n) return n;
+  uint64_t need = (k - 1) % OR_SEL_SAMPLE; /* b-bits still to skip after the sample */
+  for (; i < n; i++) {
+    uint32_t bit = (uint32_t)((B[i >> 6] >> (i & 63)) & 1u);
+    if (bit == b) {
+      if (need == 0) return i;
+      need--;
+    }
+  }
+  return n;
+}
+
+/* --- tree --- */
+int oracle_select_dir(const oracle_tree *t, uint32_t **sel0, uint32_t **sel1, uint64_t *sps_out) {
+  if (!t || !sel0 || !sel1 || !sps_out) return OR_EINVAL;
+  uint64_t sps = sel_per_level(t->n);
+  uint32_t *s0 = (uint32_t *)malloc((t->levels * sps + 1) * sizeof(uint32_t));
+  uint32_t *s1 = (uint32_t *)malloc((t->levels * sps + 1) * sizeof(uint32_t));
+  if (!s0 || !s1) { free(s0); free(s1); return OR_ENOMEM; }
+  for (uint32_t l = 0; l < t->levels; l++) {
+    const uint64_t *B = t->bits + (uint64_t)l * t->words_per_level;
+    select_samples(B, t->n, 0, s0 + (uint64_t)l * sps, sps);
+    select_samples(B, t->n, 1, s1 + (uint64_t)l * sps, sps);
+  }
+  *sel0 = s0; *sel1 = s1; *sps_out = sps;
+  return OR_OK;
+}
+
+void oracle_free_buf(void *p) { free(p); }
+
+/* select_c(S, k) on the tree: top-down node ranges [s_l, e_l) of c's prefix
+ * (as rank does), then bottom-up: the offset p inside the level-(l+1) child
+ * becomes select_b(level l, rank_b(s_l) + p + 1) - s_l. */
+uint64_t oracle_select(const oracle_tree *t, const uint32_t *sel0, const uint32_t *sel1, uint64_t sps, uint32_t c,
+                       uint64_t k) {
+  if (!t || (uint64_t)c >= t->sigma || k == 0 || k > t->n) return UINT64_MAX;
+  uint32_t L = t->levels;
+  uint64_t s[33], e[33];
+  s[0] = 0; e[0] = t->n;
+  for (uint32_t l = 0; l < L; l++) {
+    uint64_t r1s = rank1(t, l, s[l]), r1e = rank1(t, l, e[l]);
+    uint64_t z = (e[l] - s[l]) - (r1e - r1s);
+    if ((c >> (L - 1 - l)) & 1u) { s[l + 1] = s[l] + z; e[l + 1] = e[l]; }
+    else { s[l + 1] = s[l]; e[l + 1] = s[l] + z; }
+  }
+  if (k > e[L] - s[L]) return UINT64_MAX; /* fewer than k occurrences of c */
+  uint64_t p = k - 1;                      /* offset inside c's range at level L */
+  for (uint32_t l = L; l-- > 0;) {
+    const uint64_t *B = t->bits + (uint64_t)l * t->words_per_level;
+    uint32_t b = (c >> (L - 1 - l)) & 1u;
+    uint64_t before = b ? rank1(t, l, s[l]) : s[l] - rank1(t, l, s[l]);
+    uint64_t q = level_select(B, t->n, (b ? sel1 : sel0) + (uint64_t)l * sps, b, before + p + 1);
+    p = q - s[l];
+  }
+  return p;
+}
+
+/* --- matrix --- */
+int oracle_wm_select_dir(const oracle_wm *m, uint32_t **sel0, uint32_t **sel1, uint64_t *sps_out) {
+  if (!m || !sel0 || !sel1 || !sps_out) return OR_EINVAL;
+  uint64_t sps = sel_per_level(m->n);
+  uint32_t *s0 = (uint32_t *)malloc((m->levels * sps + 1) * sizeof(uint32_t));
+  uint32_t *s1 = (uint32_t *)malloc((m->levels * sps + 1) * sizeof(uint32_t));
+  if (!s0 || !s1) { free(s0); free(s1); return OR_ENOMEM; }
+  for (uint32_t l = 0; l < m->levels; l++) {
+    const uint64_t *B = m->bits + (uint64_t)l * m->words_per_level;
+    select_samples(B, m->n, 0, s0 + (uint64_t)l * sps, sps);
+    select_samples(B, m->n, 1, s1 + (uint64_t)l * sps, sps);
+  }
+  *sel0 = s0; *sel1 = s1; *sps_out = sps;
+  return OR_OK;
+}
+
+/* select_c on the matrix: c's class start at every level top-down
+ * (s_{l+1} = b ? zeros[l] + rank1(s_l) : rank0(s_l)), then bottom-up
+ * p_l = select_b(level l, rank_b(s_l) + (p_{l+1} - s_{l+1}) + 1). */
+uint64_t oracle_wm_select(const oracle_wm *m, const uint32_t *sel0, const uint32_t *sel1, uint64_t sps, uint32_t c,
+                          uint64_t k) {
+  if (!m || (uint64_t)c >= m->sigma || k == 0 || k > m->n) return UINT64_MAX;
+  uint32_t L = m->levels;
+  uint64_t s[33], e[33];
+  s[0] = 0; e[0] = m->n;
+  for (uint32_t l = 0; l < L; l++) {
+    uint64_t r1s = wm_rank1(m, l, s[l]), r1e = wm_rank1(m, l, e[l]);
+    if ((c >> (L - 1 - l)) & 1u) { s[l + 1] = m->zeros[l] + r1s; e[l + 1] = m->zeros[l] + r1e; }
+    else { s[l + 1] = s[l] - r1s; e[l + 1] = e[l] - r1e; }
+  }
+  if (k > e[L] - s[L]) return UINT64_MAX;
+  uint64_t p = s[L] + k - 1; /* position at the (virtual) level L */
+  for (uint32_t l = L; l-- > 0;) {
+    const uint64_t *B = m->bits + (uint64_t)l * m->words_per_level;
+    uint32_t b = (c >> (L - 1 - l)) & 1u;
+    uint64_t r1s = wm_rank1(m, l, s[l]);
+    uint64_t before = b ? r1s : s[l] - r1s;
+    uint64_t off = p - s[l + 1];
+    p = level_select(B, m->n, (b ? sel1 : sel0) + (uint64_t)l * sps, b, before + off + 1);
+  }
+  return p;
+}
