@@ -69,6 +69,9 @@ typedef struct wt_tree {
   uint64_t supers_per_level;  /* ceil(n/65536) + 1                            */
   uint16_t *rank_block;       /* u16[levels * blocks_per_level]               */
   uint64_t *rank_super;       /* u64[levels * supers_per_level]               */
+  uint64_t select_per_level;  /* ceil(n/4096) + 1 (0 until wt_select_index)   */
+  uint32_t *select0;          /* u32[levels * select_per_level] or NULL       */
+  uint32_t *select1;          /* u32[levels * select_per_level] or NULL       */
   void *internal;             /* library bookkeeping; do not touch            */
 } wt_tree;
 
@@ -146,6 +149,9 @@ typedef struct wm_matrix {
   uint64_t supers_per_level;  /* ceil(n/65536) + 1                            */
   uint16_t *rank_block;       /* u16[levels * blocks_per_level] (device)      */
   uint64_t *rank_super;       /* u64[levels * supers_per_level] (device)      */
+  uint64_t select_per_level;  /* as wt_tree                                   */
+  uint32_t *select0;
+  uint32_t *select1;
   void *internal;             /* library bookkeeping; do not touch            */
 } wm_matrix;
 
@@ -163,6 +169,30 @@ int wm_free(wm_matrix *m);
 int wm_access(const wm_matrix *m, const uint64_t *d_pos, uint64_t q, uint32_t *d_out, void *stream);
 int wm_rank(const wm_matrix *m, const uint32_t *d_sym, const uint64_t *d_pos, uint64_t q,
             uint64_t *d_out, void *stream);
+
+/* ---- select ----
+ *
+ * Select directory (Clark's first level; DESIGN.md reading
+ * R-14): per level, the positions of every 4096'th 0 bit and 1 bit --
+ * select1[l*SPS + j] = position of the (4096 j)'th 1 bit of level l (0-based
+ * count), select0 likewise for 0 bits, SPS = ceil(n/4096) + 1, entries past
+ * the last sample are n.  Built on demand (the paper times construction
+ * without rank/select, :649-651) by *_select_index, asynchronously on
+ * `stream`, owned by the tree / matrix and released with it; idempotent.
+ *
+ * wt_select / wm_select -- batched select_c(S, k) = position of the k'th
+ * (k >= 1) occurrence of symbol c.  d_sym: DEVICE u32[q]; d_k: DEVICE
+ * u64[q]; d_out: DEVICE u64[q] receives the 0-based position, or UINT64_MAX
+ * when k == 0, k exceeds the count of c, or c >= sigma.  Asynchronous on
+ * `stream`.  WT_EINVAL on null pointers (q > 0) or when the select index
+ * has not been built.
+ */
+int wt_select_index(wt_tree *t, void *stream);
+int wt_select(const wt_tree *t, const uint32_t *d_sym, const uint64_t *d_k, uint64_t q, uint64_t *d_out,
+              void *stream);
+int wm_select_index(wm_matrix *m, void *stream);
+int wm_select(const wm_matrix *m, const uint32_t *d_sym, const uint64_t *d_k, uint64_t q, uint64_t *d_out,
+              void *stream);
 
 /* ---- measurement hooks (used by bench.py; no effect on results) ---- */
 

@@ -10,6 +10,7 @@
 #include "wt_prep.cuh"
 #include "wt_rank.cuh"
 #include "wt_wm.cuh"
+#include "wt_select.cuh"
 
 #include <cstdio>
 #include <algorithm>
@@ -965,6 +966,54 @@ int wt_last_profile(wt_profile *out) {
 
 const char *wt_version(void) { return "wt-b200 0.1 (sm_100a)"; }
 
+// select directory of one structure (bits + rank directory in `v`), stream-ordered
+static int select_index_impl(const TreeView &v, uint64_t *sps_out, uint32_t **s0, uint32_t **s1,
+                             std::vector<void *> &owned, cudaStream_t s) {
+  if (*sps_out) return WT_OK;  // already built
+  const uint64_t sps = (v.n + SEL_SAMPLE - 1) / SEL_SAMPLE + 1;
+  const uint64_t cnt = (uint64_t)v.L * sps;
+  uint32_t *a = nullptr, *b = nullptr;
+  if (cnt) {
+    if (cudaMallocAsync(&a, cnt * sizeof(uint32_t), s) != cudaSuccess) return WT_ENOMEM;
+    if (cudaMallocAsync(&b, cnt * sizeof(uint32_t), s) != cudaSuccess) {
+      cudaFreeAsync(a, s);
+      return WT_ENOMEM;
+    }
+    const unsigned fg = (unsigned)std::min<uint64_t>((cnt + 255) / 256, 65535);
+    k_fill_u32<<<fg, 256, 0, s>>>(a, cnt, (uint32_t)v.n);
+    k_fill_u32<<<fg, 256, 0, s>>>(b, cnt, (uint32_t)v.n);
+    const uint64_t items = (uint64_t)v.L * v.bpl;
+    if (items) k_select_dir<<<(unsigned)((items + 255) / 256), 256, 0, s>>>(v, a, b, sps);
+    if (cudaGetLastError() != cudaSuccess) {
+      cudaFreeAsync(a, s);
+      cudaFreeAsync(b, s);
+      return WT_ECUDA;
+    }
+    owned.push_back(a);
+    owned.push_back(b);
+  }
+  *s0 = a;
+  *s1 = b;
+  *sps_out = sps;
+  return WT_OK;
+}
+
+int wt_select_index(wt_tree *t, void *stream) {
+  if (!t || !t->internal) return WT_EINVAL;
+  Internal *in = static_cast<Internal *>(t->internal);
+  return select_index_impl(view_of(t), &t->select_per_level, &t->select0, &t->select1, in->outputs,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int wt_select(const wt_tree *t, const uint32_t *d_sym, const uint64_t *d_k, uint64_t q, uint64_t *d_out,
+              void *stream) {
+  if (!t || (q > 0 && (!d_sym || !d_k || !d_out)) || !t->select_per_level) return WT_EINVAL;
+  if (q == 0) return WT_OK;
+  k_wt_select<<<(unsigned)((q + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      view_of(t), t->select0, t->select1, t->select_per_level, t->sigma, d_sym, d_k, q, d_out);
+  return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
+}
+
 int wm_build(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma, void *stream, wm_matrix **out) {
   return wm_build_impl(d_seq, n, elem_bytes, sigma, stream, out);
 }
@@ -1004,6 +1053,22 @@ int wm_access(const wm_matrix *m, const uint64_t *d_pos, uint64_t q, uint32_t *d
   if (q == 0) return WT_OK;
   k_wm_access<<<(unsigned)((q + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(view_of_wm(m), m->zeros,
                                                                                            d_pos, q, d_out);
+  return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
+}
+
+int wm_select_index(wm_matrix *m, void *stream) {
+  if (!m || !m->internal) return WT_EINVAL;
+  WmInternal *in = static_cast<WmInternal *>(m->internal);
+  return select_index_impl(view_of_wm(m), &m->select_per_level, &m->select0, &m->select1, in->outputs,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int wm_select(const wm_matrix *m, const uint32_t *d_sym, const uint64_t *d_k, uint64_t q, uint64_t *d_out,
+              void *stream) {
+  if (!m || (q > 0 && (!d_sym || !d_k || !d_out)) || !m->select_per_level) return WT_EINVAL;
+  if (q == 0) return WT_OK;
+  k_wm_select<<<(unsigned)((q + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      view_of_wm(m), m->zeros, m->select0, m->select1, m->select_per_level, m->sigma, d_sym, d_k, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
 }
 

@@ -38,6 +38,7 @@ class _WtTree(ctypes.Structure):
         ("total_nodes", ctypes.c_uint64),
         ("blocks_per_level", ctypes.c_uint64), ("supers_per_level", ctypes.c_uint64),
         ("rank_block", ctypes.c_void_p), ("rank_super", ctypes.c_void_p),
+        ("select_per_level", ctypes.c_uint64), ("select0", ctypes.c_void_p), ("select1", ctypes.c_void_p),
         ("internal", ctypes.c_void_p),
     ]
 
@@ -72,6 +73,9 @@ class _WmMatrix(ctypes.Structure):
         ("supers_per_level", ctypes.c_uint64),
         ("rank_block", ctypes.c_void_p),
         ("rank_super", ctypes.c_void_p),
+        ("select_per_level", ctypes.c_uint64),
+        ("select0", ctypes.c_void_p),
+        ("select1", ctypes.c_void_p),
         ("internal", ctypes.c_void_p),
     ]
 
@@ -114,6 +118,12 @@ def _load():
     lib.wm_rank.argtypes = [PM, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                             ctypes.c_void_p]
     lib.wm_rank.restype = ctypes.c_int
+    for pre, PT in (("wt", P), ("wm", PM)):
+        getattr(lib, f"{pre}_select_index").argtypes = [PT, ctypes.c_void_p]
+        getattr(lib, f"{pre}_select_index").restype = ctypes.c_int
+        getattr(lib, f"{pre}_select").argtypes = [PT, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                                  ctypes.c_void_p, ctypes.c_void_p]
+        getattr(lib, f"{pre}_select").restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -139,7 +149,42 @@ def _stream_ptr(stream) -> int:
     return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
 
 
-class WaveletTree:
+class _SelectOps:
+    """select_c through the C ABI; the directory is built on
+    first use (``select_index``)."""
+    _pre = "wt"
+
+    def select_index(self, stream=None) -> dict:
+        lib = _load()
+        rc = getattr(lib, f"{self._pre}_select_index")(self.handle, ctypes.c_void_p(_stream_ptr(stream)))
+        if rc != WT_OK:
+            raise WtError(rc, f"{self._pre}_select_index")
+        h = self.handle.contents
+        sps = int(h.select_per_level)
+        cnt = self.levels * sps
+        return {"select_per_level": sps,
+                "select0": _view(h.select0, cnt, "<u4", torch.uint32, self.device),
+                "select1": _view(h.select1, cnt, "<u4", torch.uint32, self.device)}
+
+    def select(self, sym: torch.Tensor, k: torch.Tensor, stream=None) -> torch.Tensor:
+        lib = _load()
+        if not int(self.handle.contents.select_per_level):
+            self.select_index(stream)
+        sym = sym.contiguous().view(-1)
+        k = k.contiguous().view(-1)
+        if sym.numel() != k.numel():
+            raise ValueError("sym and k must have the same length")
+        out = torch.empty(k.numel(), dtype=torch.int64, device=k.device)
+        rc = getattr(lib, f"{self._pre}_select")(self.handle, ctypes.c_void_p(sym.data_ptr() if sym.numel() else 0),
+                                                 ctypes.c_void_p(k.data_ptr() if k.numel() else 0), k.numel(),
+                                                 ctypes.c_void_p(out.data_ptr() if out.numel() else 0),
+                                                 ctypes.c_void_p(_stream_ptr(stream)))
+        if rc != WT_OK:
+            raise WtError(rc, f"{self._pre}_select")
+        return out.view(torch.uint64)
+
+
+class WaveletTree(_SelectOps):
     """A built tree.  Arrays are zero-copy torch views of library memory and
     stay valid until ``free()`` (called on garbage collection too)."""
 
@@ -299,7 +344,8 @@ def version() -> str:
 
 
 # ---------------------------------------------------------------- wavelet matrix
-class WaveletMatrix:
+class WaveletMatrix(_SelectOps):
+    _pre = "wm"
     """A built wavelet matrix (PAPER.md:910-925).  Arrays are zero-copy torch
     views of library memory, valid until ``free()``."""
 
