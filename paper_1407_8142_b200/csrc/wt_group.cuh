@@ -434,6 +434,9 @@ __global__ void __launch_bounds__(WPB * 32, WT_GMINB) k_group(GroupParams p) {
       const uint32_t qlo = min((uint32_t)(warp * QL), len), qhi = min((uint32_t)((warp + 1) * QL), len);
       const uint32_t b0bit = pbits + tau - 1u;  // level-l0 bit of a key
       uint32_t ones0 = 0;
+      // the level-l0 bit of every InT lane of a 32-bit word (records = keys in the copy path)
+      const uint32_t onesmask = (sizeof(InT) == 1 ? 0x01010101u : (sizeof(InT) == 2 ? 0x00010001u : 1u)) << b0bit;
+      const bool full_digit = sizeof(InT) == 1 && pbits == 0 && ndig == 256;
       uint32_t head0;
       {
         constexpr int PER = 16 / sizeof(InT);
@@ -463,11 +466,16 @@ __global__ void __launch_bounds__(WPB * 32, WT_GMINB) k_group(GroupParams p) {
                 const InT *e = reinterpret_cast<const InT *>(&q[j]);
                 const int p0 = i * PER - head;
                 if (p0 >= (int)qlo && p0 + PER <= (int)qhi) {
+                  if (full_digit) {  // the record is the digit (u8 keys, last group): no shift or mask
 #pragma unroll
-                  for (int k = 0; k < PER; k++) {
-                    atomicAdd(&s.H[((uint32_t)e[k] >> pbits) & (ndig - 1u)], 1u);
-                    ones0 += ((uint32_t)e[k] >> b0bit) & 1u;
+                    for (int k = 0; k < PER; k++) atomicAdd(&s.H[(uint32_t)e[k]], 1u);
+                  } else {
+#pragma unroll
+                    for (int k = 0; k < PER; k++) atomicAdd(&s.H[((uint32_t)e[k] >> pbits) & (ndig - 1u)], 1u);
                   }
+                  // level-l0 ones of the 16 bytes: one masked popcount per 32-bit word
+                  ones0 += __popc(q[j].x & onesmask) + __popc(q[j].y & onesmask) + __popc(q[j].z & onesmask) +
+                           __popc(q[j].w & onesmask);
                 } else {
 #pragma unroll
                   for (int k = 0; k < PER; k++) {

@@ -379,7 +379,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     } else {
       const uint64_t warps = (uint64_t)gb.gl.grid;  // CTAs (one chain at a time each)
       static const uint64_t cpw =
-          getenv("WT_CHAINS_PER_WARP") ? strtoull(getenv("WT_CHAINS_PER_WARP"), 0, 10) : 8;
+          getenv("WT_CHAINS_PER_WARP") ? strtoull(getenv("WT_CHAINS_PER_WARP"), 0, 10) : 16;
       const uint64_t target = (n + cpw * warps - 1) / (cpw * warps);
       const uint64_t tt = gb.gl.tile;
       gb.CH = std::max<uint64_t>(tt, ((target + tt - 1) / tt) * tt);
