@@ -26,7 +26,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-OK, EINVAL, ESYMBOL, ENOMEM = 0, -1, -2, -3
+OK, EINVAL, ESYMBOL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -5
 
 
 class _Tree(ctypes.Structure):
@@ -61,6 +61,29 @@ class _WM(ctypes.Structure):
         ("supers_per_level", ctypes.c_uint64),
         ("rank_block", ctypes.POINTER(ctypes.c_uint16)),
         ("rank_super", ctypes.POINTER(ctypes.c_uint64)),
+    ]
+
+
+class _HWT(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint64),
+        ("sigma", ctypes.c_uint64),
+        ("levels", ctypes.c_uint32),
+        ("elem_bytes", ctypes.c_uint32),
+        ("level_len", ctypes.POINTER(ctypes.c_uint64)),
+        ("level_word_ptr", ctypes.POINTER(ctypes.c_uint64)),
+        ("level_block_ptr", ctypes.POINTER(ctypes.c_uint64)),
+        ("level_super_ptr", ctypes.POINTER(ctypes.c_uint64)),
+        ("bits", ctypes.POINTER(ctypes.c_uint64)),
+        ("rank_block", ctypes.POINTER(ctypes.c_uint16)),
+        ("rank_super", ctypes.POINTER(ctypes.c_uint64)),
+        ("level_node_ptr", ctypes.POINTER(ctypes.c_uint64)),
+        ("node_key", ctypes.POINTER(ctypes.c_uint32)),
+        ("node_start", ctypes.POINTER(ctypes.c_uint32)),
+        ("total_nodes", ctypes.c_uint64),
+        ("code", ctypes.POINTER(ctypes.c_uint32)),
+        ("code_len", ctypes.POINTER(ctypes.c_uint8)),
+        ("only_symbol", ctypes.c_uint32),
     ]
 
 
@@ -117,6 +140,15 @@ def _load():
             lib.oracle_wm_select.argtypes = [ctypes.POINTER(_WM), U32P, U32P, ctypes.c_uint64, ctypes.c_uint32,
                                              ctypes.c_uint64]
             lib.oracle_wm_select.restype = ctypes.c_uint64
+            lib.oracle_hwt_build.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
+                                             ctypes.c_uint64, ctypes.POINTER(ctypes.POINTER(_HWT))]
+            lib.oracle_hwt_build.restype = ctypes.c_int
+            lib.oracle_hwt_free.argtypes = [ctypes.POINTER(_HWT)]
+            lib.oracle_hwt_free.restype = None
+            lib.oracle_hwt_access.argtypes = [ctypes.POINTER(_HWT), ctypes.c_uint64]
+            lib.oracle_hwt_access.restype = ctypes.c_uint32
+            lib.oracle_hwt_rank.argtypes = [ctypes.POINTER(_HWT), ctypes.c_uint32, ctypes.c_uint64]
+            lib.oracle_hwt_rank.restype = ctypes.c_uint64
             _lib = lib
     return _lib
 
@@ -327,4 +359,76 @@ def wm_build(seq: np.ndarray, sigma: int) -> dict:
         out.update(m.select_dir())
         out.update(n=m.n, sigma=m.sigma, levels=m.levels, words_per_level=m.words_per_level,
                    blocks_per_level=m.blocks_per_level, supers_per_level=m.supers_per_level)
+    return out
+
+
+class OracleHWT:
+    """Owns one C oracle Huffman-shaped wavelet tree."""
+
+    def __init__(self, seq: np.ndarray, sigma: int):
+        lib = _load()
+        seq = np.ascontiguousarray(seq)
+        if seq.dtype not in (np.uint8, np.uint16, np.uint32):
+            raise TypeError("seq must be uint8/uint16/uint32")
+        out = ctypes.POINTER(_HWT)()
+        rc = lib.oracle_hwt_build(seq.ctypes.data if seq.size else None, seq.size,
+                                  seq.dtype.itemsize, int(sigma), ctypes.byref(out))
+        if rc != OK:
+            raise OracleError(rc)
+        self._lib = lib
+        self._t = out
+        t = out.contents
+        self.n, self.sigma, self.levels = t.n, t.sigma, t.levels
+        self.total_nodes = t.total_nodes
+        self.only_symbol = t.only_symbol
+
+    def arrays(self) -> dict:
+        t = self._t.contents
+        h = t.levels
+        wp = _copy(t.level_word_ptr, h + 1, np.uint64)
+        bp = _copy(t.level_block_ptr, h + 1, np.uint64)
+        sp = _copy(t.level_super_ptr, h + 1, np.uint64)
+        return {
+            "level_len": _copy(t.level_len, h, np.uint64),
+            "level_word_ptr": wp,
+            "level_block_ptr": bp,
+            "level_super_ptr": sp,
+            "bits": _copy(t.bits, int(wp[-1]), np.uint64),
+            "rank_block": _copy(t.rank_block, int(bp[-1]), np.uint16),
+            "rank_super": _copy(t.rank_super, int(sp[-1]), np.uint64),
+            "level_node_ptr": _copy(t.level_node_ptr, h + 1, np.uint64),
+            "node_key": _copy(t.node_key, t.total_nodes, np.uint32),
+            "node_start": _copy(t.node_start, t.total_nodes, np.uint32),
+            "code": _copy(t.code, t.sigma, np.uint32),
+            "code_len": _copy(t.code_len, t.sigma, np.uint8),
+        }
+
+    def access(self, positions) -> np.ndarray:
+        return np.array([self._lib.oracle_hwt_access(self._t, int(i)) for i in positions], dtype=np.uint32)
+
+    def rank(self, symbols, positions) -> np.ndarray:
+        return np.array([self._lib.oracle_hwt_rank(self._t, int(c), int(i))
+                         for c, i in zip(symbols, positions)], dtype=np.uint64)
+
+    def close(self):
+        if getattr(self, "_t", None):
+            self._lib.oracle_hwt_free(self._t)
+            self._t = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def hwt_build(seq: np.ndarray, sigma: int) -> dict:
+    """Oracle Huffman-shaped wavelet tree; arrays as include/wt.h's hwt_tree."""
+    with OracleHWT(seq, sigma) as t:
+        out = t.arrays()
+        out.update(n=t.n, sigma=t.sigma, levels=t.levels, total_nodes=t.total_nodes,
+                   only_symbol=t.only_symbol)
     return out

@@ -41,6 +41,7 @@
 #define OR_EINVAL (-1)
 #define OR_ESYMBOL (-2)
 #define OR_ENOMEM (-3)
+#define OR_EUNSUPPORTED (-5)
 
 typedef struct {
   uint64_t n;
@@ -613,4 +614,408 @@ uint64_t oracle_wm_select(const oracle_wm *m, const uint32_t *sel0, const uint32
     p = level_select(B, m->n, (b ? sel1 : sel0) + (uint64_t)l * sps, b, before + off + 1);
   }
   return p;
+}
+
+/* ======================================================================
+ * Huffman-shaped wavelet tree (§7 "Extensions"; SURVEY
+ * §8(f) f3).
+ *
+ *   "each node is placed at a level proportional to the length of its
+ *    Huffman code" (:855-856); "we first compute the Huffman tree and
+ *    prefix codes" (:858-859); "We map each symbol to an integer
+ *    corresponding to the location of its leaf in an in-order traversal of
+ *    the Huffman tree ... At each internal node ... we store the highest
+ *    mapped integer of nodes in its left sub-tree ... the decision of how to
+ *    set the bitmap and where to place the symbol in S' can be made with a
+ *    single comparison with the mapped integers.  The rest of the
+ *    computation follows the logic of levelWT." (:862-873)
+ *
+ * Readings (R-17..R-20):
+ *   R-17 Huffman tree: the textbook two-queue construction over the symbols
+ *        that occur, leaves ordered by (frequency, symbol) ascending; each
+ *        step removes the two lightest items, a leaf before an internal
+ *        node of equal weight.  Code lengths = leaf depths.
+ *   R-18 Codes: canonical codes for those lengths (symbols ordered by
+ *        (length, symbol); the first code is all zeros; each next code is
+ *        (previous + 1) shifted left by the length increase).  The
+ *        wavelet tree has the shape of the canonical code trie; a 0 code
+ *        bit goes left (:220-224).
+ *   R-19 Levels: level l holds, for every element still inside an internal
+ *        node at depth l, its code bit l; elements whose leaf is reached
+ *        leave the sequence (levelWT's S' keeps only internal children).
+ *        Nodes in each level in left-to-right (key) order; node key = the
+ *        l-bit code prefix.  Each level's bitmap, directory and node list
+ *        use the same per-level layout as the balanced tree, with levels
+ *        concatenated (word/block/super offsets per level).
+ *   R-20 Fewer than two distinct symbols: the root is a leaf, 0 levels.
+ * ====================================================================== */
+typedef struct {
+  uint64_t n;
+  uint64_t sigma;
+  uint32_t levels;          /* h = longest code length                     */
+  uint32_t elem_bytes;
+  uint64_t *level_len;      /* levels: n_l = elements inside depth-l nodes */
+  uint64_t *level_word_ptr; /* levels + 1: ceil(n_l/512)*8 words per level  */
+  uint64_t *level_block_ptr;/* levels + 1: ceil(n_l/512) blocks per level   */
+  uint64_t *level_super_ptr;/* levels + 1: ceil(n_l/65536)+1 per level      */
+  uint64_t *bits;
+  uint16_t *rank_block;
+  uint64_t *rank_super;
+  uint64_t *level_node_ptr; /* levels + 1 */
+  uint32_t *node_key;       /* l-bit code prefix of the internal node      */
+  uint32_t *node_start;     /* first position of the node in its level     */
+  uint64_t total_nodes;
+  uint32_t *code;           /* sigma: canonical code (right-aligned)       */
+  uint8_t *code_len;        /* sigma: code length, 0 = symbol absent       */
+  uint32_t only_symbol;     /* levels == 0 and n > 0: the one symbol (R-20) */
+} oracle_hwt;
+
+/* explicit binary tree node (Huffman tree, then the canonical trie) */
+typedef struct {
+  uint64_t weight;
+  int32_t child[2];  /* -1 for a leaf */
+  int32_t sym;       /* leaf symbol, -1 for internal */
+  uint32_t thr;      /* internal: highest mapped integer of the left subtree */
+  uint64_t start;    /* internal: first position at its level */
+} or_hnode;
+
+void oracle_hwt_free(oracle_hwt *t) {
+  if (!t) return;
+  free(t->level_len); free(t->level_word_ptr); free(t->level_block_ptr); free(t->level_super_ptr);
+  free(t->bits); free(t->rank_block); free(t->rank_super);
+  free(t->level_node_ptr); free(t->node_key); free(t->node_start);
+  free(t->code); free(t->code_len);
+  free(t);
+}
+
+static int cmp_leaf(const void *a, const void *b) {
+  /* (frequency, symbol) ascending; entries are (freq << 32 | sym) */
+  uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* depth of every leaf under node v (recursive walk) */
+static void leaf_depths(const or_hnode *T, int32_t v, uint32_t d, uint8_t *len, uint32_t *maxd) {
+  if (T[v].sym >= 0) {
+    len[T[v].sym] = (uint8_t)(d > 255 ? 255 : d);
+    if (d > *maxd) *maxd = d;
+    return;
+  }
+  leaf_depths(T, T[v].child[0], d + 1, len, maxd);
+  leaf_depths(T, T[v].child[1], d + 1, len, maxd);
+}
+
+/* R-17: two-queue Huffman construction; writes len[sym] (0 = absent) and
+ * returns the longest length.  m = number of occurring symbols. */
+static int huffman_lengths(const uint64_t *freq, uint64_t sigma, uint8_t *len, uint32_t *h_out) {
+  uint64_t m = 0;
+  for (uint64_t c = 0; c < sigma; c++) m += freq[c] > 0;
+  memset(len, 0, sigma);
+  *h_out = 0;
+  if (m < 2) return 0; /* R-20 */
+  uint64_t *leaf = (uint64_t *)malloc(m * sizeof(uint64_t));
+  or_hnode *T = (or_hnode *)malloc((2 * m) * sizeof(or_hnode));
+  if (!leaf || !T) { free(leaf); free(T); return -1; }
+  uint64_t k = 0;
+  for (uint64_t c = 0; c < sigma; c++)
+    if (freq[c]) leaf[k++] = (freq[c] << 32) | c;
+  qsort(leaf, m, sizeof(uint64_t), cmp_leaf);
+  for (uint64_t i = 0; i < m; i++) {
+    T[i].weight = leaf[i] >> 32;
+    T[i].sym = (int32_t)(leaf[i] & 0xffffffffu);
+    T[i].child[0] = T[i].child[1] = -1;
+  }
+  /* queue 1 = leaves [lq, m); queue 2 = internal nodes [iq, nint) */
+  uint64_t lq = 0, iq = m, nint = m;
+  for (uint64_t step = 0; step + 1 < m; step++) {
+    int32_t pick[2];
+    for (int j = 0; j < 2; j++) {
+      int take_leaf;
+      if (lq >= m) take_leaf = 0;
+      else if (iq >= nint) take_leaf = 1;
+      else take_leaf = T[lq].weight <= T[iq].weight; /* a leaf first on ties */
+      pick[j] = (int32_t)(take_leaf ? lq++ : iq++);
+    }
+    T[nint].weight = T[pick[0]].weight + T[pick[1]].weight;
+    T[nint].child[0] = pick[0];
+    T[nint].child[1] = pick[1];
+    T[nint].sym = -1;
+    nint++;
+  }
+  leaf_depths(T, (int32_t)(nint - 1), 0, len, h_out);
+  free(leaf);
+  free(T);
+  return 0;
+}
+
+/* R-18: canonical codes from the lengths */
+static void canonical_codes(const uint8_t *len, uint64_t sigma, uint32_t h, uint32_t *code) {
+  memset(code, 0, sigma * sizeof(uint32_t));
+  uint64_t cur = 0;
+  uint32_t prev = 0;
+  int first = 1;
+  for (uint32_t L = 1; L <= h; L++) {
+    for (uint64_t c = 0; c < sigma; c++) {
+      if (len[c] != L) continue;
+      if (first) { cur = 0; first = 0; }
+      else cur = (cur + 1) << (L - prev);
+      prev = L;
+      code[c] = (uint32_t)cur;
+    }
+  }
+}
+
+/* in-order numbering of the trie: leaves get 0, 1, 2, ...; every internal
+ * node records the highest number in its left subtree (:864-869) */
+static uint32_t inorder_map(or_hnode *T, int32_t v, uint32_t next, uint32_t *map) {
+  if (T[v].sym >= 0) { map[T[v].sym] = next; return next + 1; }
+  next = inorder_map(T, T[v].child[0], next, map);
+  T[v].thr = next - 1;
+  return inorder_map(T, T[v].child[1], next, map);
+}
+
+int oracle_hwt_build(const void *seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma, oracle_hwt **out) {
+  if (!out) return OR_EINVAL;
+  *out = NULL;
+  if ((n > 0 && !seq) || (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4))
+    return OR_EINVAL;
+  if (sigma < 1 || sigma > ((uint64_t)1 << (8 * elem_bytes)) || sigma > 65536 || n >= ((uint64_t)1 << 32))
+    return OR_EINVAL;
+  uint32_t *S = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint64_t *freq = (uint64_t *)calloc(sigma, sizeof(uint64_t));
+  if (!S || !freq) { free(S); free(freq); return OR_ENOMEM; }
+  for (uint64_t i = 0; i < n; i++) {
+    uint32_t v;
+    if (elem_bytes == 1) v = ((const uint8_t *)seq)[i];
+    else if (elem_bytes == 2) v = ((const uint16_t *)seq)[i];
+    else v = ((const uint32_t *)seq)[i];
+    if ((uint64_t)v >= sigma) { free(S); free(freq); return OR_ESYMBOL; }
+    S[i] = v;
+    freq[v]++;
+  }
+  oracle_hwt *t = (oracle_hwt *)calloc(1, sizeof(oracle_hwt));
+  if (!t) { free(S); free(freq); return OR_ENOMEM; }
+  t->n = n;
+  t->sigma = sigma;
+  t->elem_bytes = elem_bytes;
+  t->code = (uint32_t *)calloc(sigma, sizeof(uint32_t));
+  t->code_len = (uint8_t *)calloc(sigma, 1);
+  uint32_t h = 0;
+  if (!t->code || !t->code_len || huffman_lengths(freq, sigma, t->code_len, &h)) {
+    free(S); free(freq); oracle_hwt_free(t);
+    return OR_ENOMEM;
+  }
+  if (h > 32) { free(S); free(freq); oracle_hwt_free(t); return OR_EUNSUPPORTED; }
+  canonical_codes(t->code_len, sigma, h, t->code);
+  t->levels = h;
+  for (uint64_t c = 0; c < sigma; c++)
+    if (freq[c]) { t->only_symbol = (uint32_t)c; break; }
+
+  /* the canonical trie: insert every code; node 0 is the root */
+  uint64_t m = 0;
+  for (uint64_t c = 0; c < sigma; c++) m += t->code_len[c] > 0;
+  uint64_t cap = 2 * (m ? m : 1);
+  or_hnode *T = (or_hnode *)calloc(cap, sizeof(or_hnode));
+  uint32_t *map = (uint32_t *)calloc(sigma, sizeof(uint32_t));
+  if (!T || !map) { free(T); free(map); free(S); free(freq); oracle_hwt_free(t); return OR_ENOMEM; }
+  uint64_t nn = 1;
+  T[0].child[0] = T[0].child[1] = -1;
+  T[0].sym = -1;
+  for (uint64_t c = 0; c < sigma && h > 0; c++) {
+    uint32_t L = t->code_len[c];
+    if (!L) continue;
+    int32_t v = 0;
+    for (uint32_t d = 0; d < L; d++) {
+      uint32_t b = (t->code[c] >> (L - 1 - d)) & 1u;
+      if (T[v].child[b] < 0) {
+        T[nn].child[0] = T[nn].child[1] = -1;
+        T[nn].sym = -1;
+        T[v].child[b] = (int32_t)nn++;
+      }
+      v = T[v].child[b];
+    }
+    T[v].sym = (int32_t)c;
+  }
+  if (h > 0) inorder_map(T, 0, 0, map);
+
+  /* levelWT over the Huffman shape (:870-873, R-19): breadth first, level by level */
+  t->level_len = (uint64_t *)calloc(h ? h : 1, sizeof(uint64_t));
+  t->level_word_ptr = (uint64_t *)calloc(h + 1, sizeof(uint64_t));
+  t->level_block_ptr = (uint64_t *)calloc(h + 1, sizeof(uint64_t));
+  t->level_super_ptr = (uint64_t *)calloc(h + 1, sizeof(uint64_t));
+  t->level_node_ptr = (uint64_t *)calloc(h + 1, sizeof(uint64_t));
+  uint32_t *A = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t)); /* mapped integers of level l */
+  uint32_t *Anext = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint32_t *X = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+  int32_t *cur = (int32_t *)malloc(cap * sizeof(int32_t)), *nxt = (int32_t *)malloc(cap * sizeof(int32_t));
+  uint32_t *ckey = (uint32_t *)malloc(cap * sizeof(uint32_t)), *nkey = (uint32_t *)malloc(cap * sizeof(uint32_t));
+  uint64_t *clen = (uint64_t *)malloc(cap * sizeof(uint64_t)), *nlen = (uint64_t *)malloc(cap * sizeof(uint64_t));
+  node_list *nodes = (node_list *)calloc(h ? h : 1, sizeof(node_list));
+  uint64_t **lbits = (uint64_t **)calloc(h ? h : 1, sizeof(uint64_t *));
+  int oom = !t->level_len || !t->level_word_ptr || !t->level_block_ptr || !t->level_super_ptr ||
+            !t->level_node_ptr || !A || !Anext || !X || !cur || !nxt || !ckey || !nkey || !clen || !nlen ||
+            !nodes || !lbits;
+  uint64_t ncur = 0, nl = n;
+  if (!oom && h > 0 && n > 0) {
+    for (uint64_t i = 0; i < n; i++) A[i] = map[S[i]];
+    cur[0] = 0; ckey[0] = 0; clen[0] = n; ncur = 1;
+  }
+  for (uint32_t l = 0; l < h && !oom; l++) {
+    t->level_len[l] = nl;
+    uint64_t wl = (nl + 511) / 512 * 8;
+    lbits[l] = (uint64_t *)calloc(wl ? wl : 1, sizeof(uint64_t));
+    if (!lbits[l]) { oom = 1; break; }
+    uint64_t pos = 0, nnext = 0, nout = 0;
+    for (uint64_t j = 0; j < ncur; j++) {
+      const or_hnode *v = &T[cur[j]];
+      uint64_t s = pos, len = clen[j];
+      if (push_node(&nodes[l], ckey[j], (uint32_t)s)) { oom = 1; break; }
+      T[cur[j]].start = s;
+      /* Fig. 1 l.12-14 with the comparison of :870-872: X[i] = 1 when the
+       * mapped integer is at most thr (the symbol is in the left subtree) */
+      uint64_t Xs = 0;
+      for (uint64_t i = 0; i < len; i++) {
+        X[s + i] = (uint32_t)Xs;
+        Xs += A[s + i] <= v->thr;
+      }
+      /* children (Fig. 1 l.18-19): only internal children continue to level l+1 */
+      const int32_t cl = v->child[0], cr = v->child[1];
+      const int keep_l = T[cl].sym < 0 && Xs > 0, keep_r = T[cr].sym < 0 && len - Xs > 0;
+      const uint64_t lbase = nout, rbase = nout + (keep_l ? Xs : 0);
+      /* Fig. 1 l.15-17: set the bit; a left symbol goes to X[i], a right one to X_s + i - X[i] */
+      for (uint64_t i = 0; i < len; i++) {
+        uint32_t a = A[s + i];
+        if (a > v->thr) {
+          lbits[l][(s + i) >> 6] |= (uint64_t)1 << ((s + i) & 63);
+          if (keep_r) Anext[rbase + i - X[s + i]] = a;
+        } else if (keep_l) {
+          Anext[lbase + X[s + i]] = a;
+        }
+      }
+      if (keep_l) { nxt[nnext] = cl; nkey[nnext] = 2 * ckey[j]; nlen[nnext] = Xs; nnext++; }
+      if (keep_r) { nxt[nnext] = cr; nkey[nnext] = 2 * ckey[j] + 1; nlen[nnext] = len - Xs; nnext++; }
+      nout += (keep_l ? Xs : 0) + (keep_r ? len - Xs : 0);
+      pos += len;
+    }
+    { uint32_t *tmp = A; A = Anext; Anext = tmp; }
+    { int32_t *tmp = cur; cur = nxt; nxt = tmp; }
+    { uint32_t *tmp = ckey; ckey = nkey; nkey = tmp; }
+    { uint64_t *tmp = clen; clen = nlen; nlen = tmp; }
+    ncur = nnext;
+    nl = nout;
+  }
+  free(A); free(Anext); free(X); free(cur); free(nxt); free(ckey); free(nkey); free(clen); free(nlen);
+  free(S); free(freq); free(map); free(T);
+
+  if (!oom) {
+    for (uint32_t l = 0; l < h; l++) {
+      uint64_t nlv = t->level_len[l];
+      t->level_word_ptr[l + 1] = t->level_word_ptr[l] + (nlv + 511) / 512 * 8;
+      t->level_block_ptr[l + 1] = t->level_block_ptr[l] + (nlv + 511) / 512;
+      t->level_super_ptr[l + 1] = t->level_super_ptr[l] + (nlv + 65535) / 65536 + 1;
+      t->level_node_ptr[l + 1] = t->level_node_ptr[l] + nodes[l].len;
+    }
+    t->total_nodes = t->level_node_ptr[h];
+    t->bits = (uint64_t *)calloc(t->level_word_ptr[h] + 1, sizeof(uint64_t));
+    t->rank_block = (uint16_t *)calloc(t->level_block_ptr[h] + 1, sizeof(uint16_t));
+    t->rank_super = (uint64_t *)calloc(t->level_super_ptr[h] + 1, sizeof(uint64_t));
+    t->node_key = (uint32_t *)malloc((t->total_nodes + 1) * sizeof(uint32_t));
+    t->node_start = (uint32_t *)malloc((t->total_nodes + 1) * sizeof(uint32_t));
+    oom = !t->bits || !t->rank_block || !t->rank_super || !t->node_key || !t->node_start;
+  }
+  for (uint32_t l = 0; l < h; l++) {
+    if (!oom) {
+      uint64_t wl = t->level_word_ptr[l + 1] - t->level_word_ptr[l];
+      if (wl) memcpy(t->bits + t->level_word_ptr[l], lbits[l], wl * sizeof(uint64_t));
+      uint64_t off = t->level_node_ptr[l];
+      if (nodes[l].len) {
+        memcpy(t->node_key + off, nodes[l].key, nodes[l].len * sizeof(uint32_t));
+        memcpy(t->node_start + off, nodes[l].start, nodes[l].len * sizeof(uint32_t));
+      }
+      rank_directory(t->bits + t->level_word_ptr[l], 1, wl, t->level_block_ptr[l + 1] - t->level_block_ptr[l],
+                     t->level_super_ptr[l + 1] - t->level_super_ptr[l], t->rank_block + t->level_block_ptr[l],
+                     t->rank_super + t->level_super_ptr[l]);
+    }
+    free(lbits[l]);
+    free(nodes[l].key);
+    free(nodes[l].start);
+  }
+  free(lbits);
+  free(nodes);
+  if (oom) { oracle_hwt_free(t); return OR_ENOMEM; }
+  *out = t;
+  return OR_OK;
+}
+
+/* rank1 of level l of the Huffman-shaped tree: ones in [0, i) */
+static uint64_t hwt_rank1(const oracle_hwt *t, uint32_t l, uint64_t i) {
+  const uint64_t nl = t->level_len[l];
+  const uint64_t *sup = t->rank_super + t->level_super_ptr[l];
+  if (i >= nl) return sup[t->level_super_ptr[l + 1] - t->level_super_ptr[l] - 1];
+  const uint64_t *B = t->bits + t->level_word_ptr[l];
+  uint64_t r = sup[i >> 16] + t->rank_block[t->level_block_ptr[l] + (i >> 9)];
+  for (uint64_t w = (i >> 9) * 8; w < (i >> 6); w++) r += popcount64(B[w]);
+  if (i & 63) r += popcount64(B[i >> 6] & (((uint64_t)1 << (i & 63)) - 1));
+  return r;
+}
+
+/* node of level l with key p: (start, end) by a linear scan of the level's list */
+static int hwt_node(const oracle_hwt *t, uint32_t l, uint32_t p, uint64_t *s, uint64_t *e) {
+  for (uint64_t j = t->level_node_ptr[l]; j < t->level_node_ptr[l + 1]; j++) {
+    if (t->node_key[j] == p) {
+      *s = t->node_start[j];
+      *e = j + 1 < t->level_node_ptr[l + 1] ? t->node_start[j + 1] : t->level_len[l];
+      return 1;
+    }
+  }
+  return 0;
+}
+
+/* the symbol whose code is the l-bit value p, or -1 */
+static int64_t hwt_leaf(const oracle_hwt *t, uint32_t l, uint32_t p) {
+  for (uint64_t c = 0; c < t->sigma; c++)
+    if (t->code_len[c] == l && t->code[c] == p) return (int64_t)c;
+  return -1;
+}
+
+/* access(i): descend; a 0 bit keeps rank0 within the node, a 1 bit rank1;
+ * stop when the code read so far is a leaf */
+uint32_t oracle_hwt_access(const oracle_hwt *t, uint64_t i) {
+  if (!t || i >= t->n) return UINT32_MAX;
+  if (t->levels == 0) return t->only_symbol; /* R-20: the root is the leaf */
+  uint32_t p = 0;
+  uint64_t s = 0, e = t->n;
+  for (uint32_t l = 0; l < t->levels; l++) {
+    const uint64_t *B = t->bits + t->level_word_ptr[l];
+    uint32_t bit = (uint32_t)((B[i >> 6] >> (i & 63)) & 1u);
+    uint64_t r1s = hwt_rank1(t, l, s), r1i = hwt_rank1(t, l, i);
+    uint64_t r = bit ? r1i - r1s : (i - s) - (r1i - r1s); /* rank within the node */
+    p = 2 * p + bit;
+    int64_t sym = hwt_leaf(t, l + 1, p);
+    if (sym >= 0) return (uint32_t)sym;
+    if (!hwt_node(t, l + 1, p, &s, &e)) return UINT32_MAX;
+    i = s + r;
+  }
+  return UINT32_MAX;
+}
+
+/* rank_c(i), inclusive: follow c's code, counting within each node */
+uint64_t oracle_hwt_rank(const oracle_hwt *t, uint32_t c, uint64_t i) {
+  if (!t || i >= t->n || (uint64_t)c >= t->sigma) return UINT64_MAX;
+  uint32_t L = t->code_len[c];
+  if (t->levels == 0) return c == t->only_symbol ? i + 1 : 0; /* R-20 */
+  if (L == 0) return 0;
+  uint64_t s = 0, e = t->n, r = i + 1;
+  uint32_t p = 0;
+  for (uint32_t l = 0; l < L; l++) {
+    uint32_t bit = (t->code[c] >> (L - 1 - l)) & 1u;
+    uint64_t r1s = hwt_rank1(t, l, s), r1p = hwt_rank1(t, l, s + r);
+    r = bit ? r1p - r1s : r - (r1p - r1s);
+    if (r == 0) return 0;
+    p = 2 * p + bit;
+    if (l + 1 == L) break;
+    if (!hwt_node(t, l + 1, p, &s, &e)) return UINT64_MAX;
+  }
+  (void)e;
+  return r;
 }

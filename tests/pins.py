@@ -162,3 +162,60 @@ def wm_access_rank_bruteforce(S: np.ndarray):
     def rank(c, i):
         return int(np.count_nonzero(S[:i + 1] == c))
     return (lambda i: int(S[i])), rank
+
+
+# ---------------------------------------------------------------------------
+# Huffman-shaped wavelet tree (R-17..R-20)
+# ---------------------------------------------------------------------------
+def huffman_cost_bruteforce(freqs) -> int:
+    """Minimum of sum f_c * len_c over all length vectors (1 <= len <= m-1)
+    satisfying Kraft's inequality -- the optimal prefix-code cost, found by
+    exhaustive enumeration (no Huffman algorithm involved)."""
+    import itertools
+    f = [int(x) for x in freqs if x > 0]
+    m = len(f)
+    if m < 2:
+        return 0
+    best = None
+    for lens in itertools.product(range(1, m), repeat=m):
+        if sum(2.0 ** -x for x in lens) <= 1.0 + 1e-12:
+            c = sum(a * b for a, b in zip(f, lens))
+            best = c if best is None or c < best else best
+    return best
+
+
+def hwt_closed_form(S, code, code_len):
+    """Levels of the Huffman-shaped tree by a sort characterisation: level l
+    holds the elements with code length > l, in S order stably sorted by
+    their l-bit code prefix; each contributes code bit l.  Node starts are
+    where the prefix changes.  Returns (per-level bit lists, per-level
+    [(key, start)] lists)."""
+    S = np.asarray(S).astype(np.int64)
+    ln = np.asarray(code_len).astype(np.int64)[S]
+    cd = np.asarray(code).astype(np.int64)[S]
+    h = int(ln.max()) if S.size else 0
+    levels, nodes = [], []
+    for l in range(h):
+        alive = np.nonzero(ln > l)[0]
+        if alive.size == 0:
+            break
+        pre = cd[alive] >> (ln[alive] - l)
+        order = np.argsort(pre, kind="stable")
+        el = alive[order]
+        bits = (cd[el] >> (ln[el] - 1 - l)) & 1
+        pl = pre[order]
+        O = np.nonzero(np.concatenate(([True], pl[1:] != pl[:-1])))[0]
+        levels.append(bits.astype(np.uint8))
+        nodes.append([(int(pl[o]), int(o)) for o in O])
+    return levels, nodes
+
+
+def rank_directory_one_level(words: np.ndarray, n: int):
+    """R-9 sampling of one level of n bits (running popcount)."""
+    BPL = (n + 511) // 512
+    SPL = (n + 65535) // 65536 + 1
+    b = np.unpackbits(words.view(np.uint8), bitorder="little")[:n].astype(np.int64)
+    pre = np.concatenate(([0], np.cumsum(b)))
+    sup = np.array([pre[min(s * 65536, n)] for s in range(SPL)], dtype=np.uint64)
+    blk = np.array([pre[k * 512] - pre[(k // 128) * 65536] for k in range(BPL)], dtype=np.uint16)
+    return blk, sup
