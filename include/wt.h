@@ -194,6 +194,77 @@ int wm_select_index(wm_matrix *m, void *stream);
 int wm_select(const wm_matrix *m, const uint32_t *d_sym, const uint64_t *d_k, uint64_t q, uint64_t *d_out,
               void *stream);
 
+/* ---- Huffman-shaped wavelet tree ----
+ *
+ * "each node is placed at a level proportional to the length of its Huffman
+ * code" (:855-856).  Readings (R-17..R-20):
+ *   - Huffman tree by the two-queue method over the occurring symbols,
+ *     leaves ordered by (frequency, symbol), a leaf before an internal node
+ *     of equal weight; code length = leaf depth (R-17).
+ *   - canonical codes: first code of length L is (first(L-1) + count(L-1))
+ *     << 1, symbols of one length numbered in symbol order (R-18); a 0 bit
+ *     goes left.  code[c] is right-aligned; code_len[c] = 0 for a symbol
+ *     that does not occur.
+ *   - level l holds, for every element whose code is longer than l, its code
+ *     bit l, in levelWT order (stable per node, nodes left to right); the
+ *     elements that reach a leaf leave the sequence (R-19).  n_l =
+ *     level_len[l]; sum_l n_l = sum_c freq(c) * code_len[c].
+ *   - fewer than two distinct symbols: 0 levels; only_symbol is the symbol
+ *     (R-20).  Codes longer than 32 bits: WT_EUNSUPPORTED.
+ * Layout: the levels are concatenated; level l occupies
+ *   bits       [level_word_ptr[l],  level_word_ptr[l+1])   ceil(n_l/512)*8 words
+ *   rank_block [level_block_ptr[l], level_block_ptr[l+1])  ceil(n_l/512)
+ *   rank_super [level_super_ptr[l], level_super_ptr[l+1])  ceil(n_l/65536)+1
+ * with the per-level meaning of wt_tree (LSB-first bits, zero padding,
+ * relative u16 block counts, absolute u64 super counts, last = level total).
+ * Nodes: CSR level_node_ptr[levels+1] over node_key (the l-bit code prefix
+ * of the internal node) and node_start (its first position in level l), in
+ * ascending key order.  Every array pointer is a DEVICE pointer owned by the
+ * library until hwt_free().
+ */
+typedef struct hwt_tree {
+  uint64_t n;                 /* sequence length                              */
+  uint64_t sigma;             /* alphabet size (<= 65536)                     */
+  uint32_t levels;            /* h = longest code length                      */
+  uint32_t elem_bytes;        /* bytes per input symbol                       */
+  uint64_t *level_len;        /* u64[levels]: n_l                             */
+  uint64_t *level_word_ptr;   /* u64[levels+1]                                */
+  uint64_t *level_block_ptr;  /* u64[levels+1]                                */
+  uint64_t *level_super_ptr;  /* u64[levels+1]                                */
+  uint64_t *bits;             /* u64[level_word_ptr[levels]]                  */
+  uint16_t *rank_block;       /* u16[level_block_ptr[levels]]                 */
+  uint64_t *rank_super;       /* u64[level_super_ptr[levels]]                 */
+  uint64_t *level_node_ptr;   /* u64[levels+1]                                */
+  uint32_t *node_key;         /* u32[total_nodes]                             */
+  uint32_t *node_start;       /* u32[total_nodes]                             */
+  uint64_t total_nodes;       /* internal nodes of the Huffman tree           */
+  uint32_t *code;             /* u32[sigma] canonical code (right-aligned)    */
+  uint8_t *code_len;          /* u8[sigma], 0 = symbol absent                 */
+  uint32_t only_symbol;       /* levels == 0 && n > 0: the single symbol      */
+  uint32_t pad_;
+  uint64_t total_bits;        /* sum of level_len                             */
+  void *internal;             /* library bookkeeping; do not touch            */
+} hwt_tree;
+
+/* hwt_build -- build the Huffman-shaped wavelet tree of S.  Arguments as
+ * wt_build with sigma <= 65536 (WT_EINVAL otherwise).  Work is enqueued on
+ * `stream`; the call synchronises it three times (after the code lengths,
+ * inside the balanced pass over the padded codes, after the node
+ * compaction).  Errors: WT_EINVAL, WT_ESYMBOL, WT_ENOMEM, WT_ECUDA,
+ * WT_EUNSUPPORTED (a code longer than 32 bits); on error *out = NULL and
+ * nothing leaks. */
+int hwt_build(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma,
+              void *stream, hwt_tree **out);
+/* hwt_free -- release everything owned by t; NULL is a no-op. */
+int hwt_free(hwt_tree *t);
+/* hwt_access / hwt_rank -- batched access(S, i) and inclusive rank_c(S, i)
+ * by descent along the code; rank_c of an absent symbol
+ * c < sigma is 0.  Buffers, sentinels and errors exactly as wt_access /
+ * wt_rank. */
+int hwt_access(const hwt_tree *t, const uint64_t *d_pos, uint64_t q, uint32_t *d_out, void *stream);
+int hwt_rank(const hwt_tree *t, const uint32_t *d_sym, const uint64_t *d_pos, uint64_t q,
+             uint64_t *d_out, void *stream);
+
 /* ---- measurement hooks (used by bench.py; no effect on results) ---- */
 
 #define WT_PROF_MAX 32

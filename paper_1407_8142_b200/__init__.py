@@ -5,8 +5,8 @@ The compute path is the C-ABI library ``libwt_b200.so`` (CUDA kernels in
 the same names: it only marshals arguments.  There is no CPU fallback: if the
 library is missing, importing ``wt`` raises.
 """
-from .wt import (WT_ESYMBOL, WaveletMatrix, WaveletTree, WtError, access, build, build_host, free,
-                 lib_path, rank, profile_enable, last_profile, version, wm_build)
+from .wt import (WT_ESYMBOL, HuffmanWaveletTree, WaveletMatrix, WaveletTree, WtError, access, build, build_host, free,
+                 lib_path, rank, profile_enable, last_profile, version, wm_build, hwt_build)
 
-__all__ = ["WT_ESYMBOL", "WaveletMatrix", "WaveletTree", "WtError", "access", "build", "build_host",
-           "free", "lib_path", "rank", "profile_enable", "last_profile", "version", "wm_build"]
+__all__ = ["WT_ESYMBOL", "HuffmanWaveletTree", "WaveletMatrix", "WaveletTree", "WtError", "access", "build", "build_host",
+           "free", "lib_path", "rank", "profile_enable", "last_profile", "version", "wm_build", "hwt_build"]

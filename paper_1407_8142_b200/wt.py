@@ -429,3 +429,137 @@ def wm_build(seq: torch.Tensor, sigma: int, stream=None) -> WaveletMatrix:
     if rc != WT_OK:
         raise WtError(rc, "wm_build")
     return WaveletMatrix(out, seq.device)
+
+
+# ------------------------------------------------------ Huffman-shaped tree
+class _HwtTree(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint64), ("sigma", ctypes.c_uint64),
+        ("levels", ctypes.c_uint32), ("elem_bytes", ctypes.c_uint32),
+        ("level_len", ctypes.c_void_p), ("level_word_ptr", ctypes.c_void_p),
+        ("level_block_ptr", ctypes.c_void_p), ("level_super_ptr", ctypes.c_void_p),
+        ("bits", ctypes.c_void_p), ("rank_block", ctypes.c_void_p), ("rank_super", ctypes.c_void_p),
+        ("level_node_ptr", ctypes.c_void_p), ("node_key", ctypes.c_void_p), ("node_start", ctypes.c_void_p),
+        ("total_nodes", ctypes.c_uint64),
+        ("code", ctypes.c_void_p), ("code_len", ctypes.c_void_p),
+        ("only_symbol", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+        ("total_bits", ctypes.c_uint64),
+        ("internal", ctypes.c_void_p),
+    ]
+
+
+def _load_hwt():
+    lib = _load()
+    if getattr(lib, "_hwt_ready", False):
+        return lib
+    PH = ctypes.POINTER(_HwtTree)
+    lib.hwt_build.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                              ctypes.c_void_p, ctypes.POINTER(PH)]
+    lib.hwt_build.restype = ctypes.c_int
+    lib.hwt_free.argtypes = [PH]
+    lib.hwt_free.restype = ctypes.c_int
+    lib.hwt_access.argtypes = [PH, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+    lib.hwt_access.restype = ctypes.c_int
+    lib.hwt_rank.argtypes = [PH, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                             ctypes.c_void_p]
+    lib.hwt_rank.restype = ctypes.c_int
+    lib._hwt_ready = True
+    return lib
+
+
+class HuffmanWaveletTree:
+    """A built Huffman-shaped wavelet tree.  Arrays are
+    zero-copy torch views of library memory, valid until ``free()``."""
+    _ARRAYS = ("level_len", "level_word_ptr", "level_block_ptr", "level_super_ptr", "bits", "rank_block",
+               "rank_super", "level_node_ptr", "node_key", "node_start", "code", "code_len")
+
+    def __init__(self, handle, device):
+        self._h = handle
+        t = handle.contents
+        self.device = device
+        self.n, self.sigma, self.levels = int(t.n), int(t.sigma), int(t.levels)
+        self.total_nodes, self.total_bits = int(t.total_nodes), int(t.total_bits)
+        self.only_symbol = int(t.only_symbol)
+        h = self.levels
+        u8 = lambda p, c: _view(p, c, "<u8", torch.uint64, device)  # noqa: E731
+        self.level_len = u8(t.level_len, h)
+        self.level_word_ptr = u8(t.level_word_ptr, h + 1)
+        self.level_block_ptr = u8(t.level_block_ptr, h + 1)
+        self.level_super_ptr = u8(t.level_super_ptr, h + 1)
+        wp, bp, sp = (int(x[-1]) if h else 0 for x in (self.level_word_ptr.cpu(), self.level_block_ptr.cpu(),
+                                                        self.level_super_ptr.cpu()))
+        self.bits = u8(t.bits, wp)
+        self.rank_block = _view(t.rank_block, bp, "<u2", torch.uint16, device)
+        self.rank_super = u8(t.rank_super, sp)
+        self.level_node_ptr = u8(t.level_node_ptr, h + 1)
+        self.node_key = _view(t.node_key, self.total_nodes, "<u4", torch.uint32, device)
+        self.node_start = _view(t.node_start, self.total_nodes, "<u4", torch.uint32, device)
+        self.code = _view(t.code, self.sigma, "<u4", torch.uint32, device)
+        self.code_len = _view(t.code_len, self.sigma, "|u1", torch.uint8, device)
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("tree already freed")
+        return self._h
+
+    def numpy(self) -> dict:
+        out = {k: getattr(self, k).cpu().numpy() for k in self._ARRAYS}
+        out.update(n=self.n, sigma=self.sigma, levels=self.levels, total_nodes=self.total_nodes,
+                   total_bits=self.total_bits, only_symbol=self.only_symbol)
+        return out
+
+    def access(self, pos: torch.Tensor, stream=None) -> torch.Tensor:
+        lib = _load_hwt()
+        pos = pos.contiguous().view(-1)
+        out = torch.empty(pos.numel(), dtype=torch.int32, device=pos.device)
+        rc = lib.hwt_access(self.handle, ctypes.c_void_p(pos.data_ptr() if pos.numel() else 0), pos.numel(),
+                            ctypes.c_void_p(out.data_ptr() if out.numel() else 0),
+                            ctypes.c_void_p(_stream_ptr(stream)))
+        if rc != WT_OK:
+            raise WtError(rc, "hwt_access")
+        return out.view(torch.uint32)
+
+    def rank(self, sym: torch.Tensor, pos: torch.Tensor, stream=None) -> torch.Tensor:
+        lib = _load_hwt()
+        sym = sym.contiguous().view(-1)
+        pos = pos.contiguous().view(-1)
+        if sym.numel() != pos.numel():
+            raise ValueError("sym and pos must have the same length")
+        out = torch.empty(pos.numel(), dtype=torch.int64, device=pos.device)
+        rc = lib.hwt_rank(self.handle, ctypes.c_void_p(sym.data_ptr() if sym.numel() else 0),
+                          ctypes.c_void_p(pos.data_ptr() if pos.numel() else 0), pos.numel(),
+                          ctypes.c_void_p(out.data_ptr() if out.numel() else 0),
+                          ctypes.c_void_p(_stream_ptr(stream)))
+        if rc != WT_OK:
+            raise WtError(rc, "hwt_rank")
+        return out.view(torch.uint64)
+
+    def free(self):
+        if self._h is not None:
+            for k in self._ARRAYS:
+                setattr(self, k, None)
+            rc = _load_hwt().hwt_free(self._h)
+            self._h = None
+            if rc != WT_OK:
+                raise WtError(rc, "hwt_free")
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def hwt_build(seq: torch.Tensor, sigma: int, stream=None) -> HuffmanWaveletTree:
+    """hwt_build on a CUDA tensor holding S (8/16/32-bit integers, read as unsigned; sigma <= 65536)."""
+    lib = _load_hwt()
+    if not seq.is_cuda:
+        raise ValueError("hwt_build() needs a CUDA tensor")
+    seq = seq.contiguous().view(-1)
+    out = ctypes.POINTER(_HwtTree)()
+    rc = lib.hwt_build(ctypes.c_void_p(seq.data_ptr() if seq.numel() else 0), seq.numel(),
+                       _elem_bytes(seq), int(sigma), ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out))
+    if rc != WT_OK:
+        raise WtError(rc, "hwt_build")
+    return HuffmanWaveletTree(out, seq.device)

@@ -14,13 +14,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "wt.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(w[tm]_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*((?:w[tm]|hwt)_\w+)\s*\(", src, flags=re.M)))
 
 
 def test_header_declares_expected_calls():
     names = _declared()
     for req in ("wt_build", "wt_build_host", "wt_free", "wt_access", "wt_rank",
-                "wm_build", "wm_free", "wm_access", "wm_rank"):
+                "wm_build", "wm_free", "wm_access", "wm_rank",
+                "hwt_build", "hwt_free", "hwt_access", "hwt_rank"):
         assert req in names
 
 
@@ -53,6 +54,14 @@ def test_null_and_argument_errors_without_gpu():
     assert lib.wm_build(None, 10, 1, 4, None, ctypes.byref(mout)) == wt.WT_EINVAL
     assert lib.wm_build(None, 0, 3, 4, None, ctypes.byref(mout)) == wt.WT_EINVAL
     assert lib.wm_free(None) == wt.WT_OK
+    hl = wt._load_hwt()
+    hout = ctypes.POINTER(wt._HwtTree)()
+    assert hl.hwt_build(None, 10, 1, 4, None, ctypes.byref(hout)) == wt.WT_EINVAL
+    assert hl.hwt_build(ctypes.c_void_p(16), 10, 4, 65537, None, ctypes.byref(hout)) == wt.WT_EINVAL
+    assert hl.hwt_build(ctypes.c_void_p(16), 10, 5, 4, None, ctypes.byref(hout)) == wt.WT_EINVAL
+    assert not hout
+    assert hl.hwt_free(None) == wt.WT_OK
+    assert hl.hwt_access(None, None, 0, None, None) == wt.WT_EINVAL
     assert lib.wt_build(ctypes.c_void_p(16), 10, 3, 4, None, ctypes.byref(out)) == wt.WT_EINVAL
     assert lib.wt_build(ctypes.c_void_p(16), 10, 1, 257, None, ctypes.byref(out)) == wt.WT_EINVAL
     assert lib.wt_build(ctypes.c_void_p(16), 10, 1, 0, None, ctypes.byref(out)) == wt.WT_EINVAL

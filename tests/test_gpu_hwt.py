@@ -1,0 +1,130 @@
+"""GPU parity of the Huffman-shaped wavelet tree (SURVEY §8(f) f3,
+PAPER.md:854-876): the CUDA path through the C ABI (hwt_build / hwt_access /
+hwt_rank) against the CPU oracle (oracle_hwt_build), bit-exact on every array
+(codes, level sizes, bitmaps, node tables, rank directories)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+KEYS = ("code", "code_len", "level_len", "level_word_ptr", "level_block_ptr", "level_super_ptr", "bits",
+        "rank_block", "rank_super", "level_node_ptr", "node_key", "node_start")
+
+
+def _dt(sigma):
+    return np.uint8 if sigma <= 256 else (np.uint16 if sigma <= 65536 else np.uint32)
+
+
+def _compare(S, sigma):
+    import paper_1407_8142_b200 as wt
+    t = wt.hwt_build(torch.from_numpy(np.ascontiguousarray(S)).cuda(), sigma)
+    got = t.numpy()
+    want = oracle.hwt_build(S, sigma)
+    assert got["levels"] == want["levels"]
+    assert got["total_nodes"] == want["total_nodes"]
+    if want["levels"] == 0 and S.size:
+        assert got["only_symbol"] == want["only_symbol"]
+    for k in KEYS:
+        assert got[k].shape == want[k].shape, f"{k} shape {got[k].shape} vs {want[k].shape}"
+        if not np.array_equal(got[k], want[k]):
+            bad = np.nonzero(got[k] != want[k])[0]
+            raise AssertionError(f"{k}: {bad.size} mismatches, first at {bad[:5]}")
+    assert got["total_bits"] == int(want["level_len"].sum())
+    return t
+
+
+def _queries(t, S, sigma, k=3000, seed=0):
+    rng = np.random.default_rng(seed)
+    n = S.size
+    pos = rng.integers(0, max(n, 1), k) if n else np.zeros(k, np.int64)
+    pos[:3] = [n, n + 5, 0]
+    sym = np.where(rng.random(k) < 0.6, S[np.minimum(pos, max(n - 1, 0))] if n else 0,
+                   rng.integers(0, sigma + 2, k)).astype(np.uint32)
+    with oracle.OracleHWT(S, sigma) as o:
+        want_a = o.access(pos)
+        want_r = o.rank(sym, pos)
+    acc = t.access(torch.from_numpy(pos.astype(np.int64)).cuda()).cpu().numpy()
+    rk = t.rank(torch.from_numpy(sym.view(np.int32)).cuda(), torch.from_numpy(pos.astype(np.int64)).cuda()).cpu().numpy()
+    assert np.array_equal(acc, want_a)
+    assert np.array_equal(rk, want_r)
+    ok = pos < n
+    if n:
+        assert np.array_equal(acc[ok], S[pos[ok]].astype(np.uint32))
+
+
+@pytest.mark.parametrize("sigma", [1, 2, 3, 5, 146, 256, 257, 1000, 8192, 8193, 65536])
+@pytest.mark.parametrize("n", [0, 1, 2, 33, 4097, 100000])
+def test_hwt_uniform(n, sigma):
+    S = gen.uniform_below(n, sigma, seed=17 * n + sigma, dtype=_dt(sigma))
+    _compare(S, sigma).free()
+
+
+@pytest.mark.parametrize("shape", ["zipf", "geometric", "fibonacci", "constant", "two", "sorted", "sparse"])
+def test_hwt_shapes(shape):
+    rng = np.random.default_rng(5)
+    sigma = 256
+    if shape == "zipf":
+        S = gen.zipf_permuted(300000, 11)
+    elif shape == "geometric":
+        S = np.minimum(rng.geometric(0.2, 200000) - 1, 255).astype(np.uint8)
+    elif shape == "fibonacci":  # path-shaped tree, depth 24
+        fib = [1, 1]
+        while len(fib) < 25:
+            fib.append(fib[-1] + fib[-2])
+        S = np.repeat(np.arange(25, dtype=np.uint8), fib)
+        rng.shuffle(S)
+    elif shape == "constant":
+        S = np.full(5000, 77, np.uint8)
+    elif shape == "two":
+        S = (rng.random(10000) < 0.01).astype(np.uint8) * 200
+    elif shape == "sorted":
+        S = np.sort(gen.zipf_permuted(100000, 2))
+    else:  # few symbols spread over a large alphabet
+        S = rng.choice(np.array([3, 900, 40000, 65535], np.uint32), 50000, p=[0.7, 0.2, 0.07, 0.03]).astype(np.uint32)
+        sigma = 65536
+    t = _compare(S, sigma)
+    _queries(t, S, sigma)
+    t.free()
+
+
+def test_hwt_queries_u16():
+    S = gen.uniform_below(150000, 3000, seed=8, dtype=np.uint16)
+    t = _compare(S, 3000)
+    _queries(t, S, 3000, k=5000, seed=3)
+    t.free()
+
+
+def test_hwt_errors():
+    import paper_1407_8142_b200 as wt
+    with pytest.raises(wt.WtError) as e:
+        wt.hwt_build(torch.tensor([0, 1, 5, 2], dtype=torch.uint8).cuda(), 4)
+    assert e.value.code == wt.WT_ESYMBOL
+    with pytest.raises(wt.WtError) as e:
+        wt.hwt_build(torch.tensor([0, 1], dtype=torch.int32).cuda(), 1 << 17)
+    assert e.value.code == -1
+
+
+def test_hwt_too_deep():
+    # 34 Fibonacci weights: a 33-bit code (R-20) -> WT_EUNSUPPORTED, nothing leaks
+    import paper_1407_8142_b200 as wt
+    fib = [1, 1]
+    while len(fib) < 34:
+        fib.append(fib[-1] + fib[-2])
+    S = torch.from_numpy(np.repeat(np.arange(34, dtype=np.uint8), fib)).cuda()
+    with pytest.raises(wt.WtError) as e:
+        wt.hwt_build(S, 34)
+    assert e.value.code == -5
+
+
+@pytest.mark.parametrize("cfg_idx", [1, 2, 3])
+def test_hwt_full_config(cfg_idx):
+    cfg = gen.CONFIGS[cfg_idx]
+    S = gen.config_input(cfg)
+    t = _compare(S, cfg.sigma)
+    _queries(t, S, cfg.sigma, k=2000, seed=cfg_idx)
+    t.free()
