@@ -10,10 +10,13 @@ node table, all 16 levels of bitmaps with the fused splits, rank directory)
 plus wt_free.  Inputs (1 GiB) are larger than the 126 MB L2, so no explicit
 flush is needed between steps.
 
-Multi-GPU (torchrun): "replicas only" -- the build does not shard in this
-round; each rank builds its own independent tree of
-the same configuration (seed + rank), value = all ranks' symbol-levels /
-max-over-ranks time, scaling "weak".
+Multi-GPU (torchrun): by default replicas -- each rank builds its own
+independent tree of the same configuration (seed + rank), value = all ranks'
+symbol-levels / max-over-ranks time, scaling "weak".  --sharded runs the
+sharded build instead (paper_1407_8142_b200/dist.py): the
+config's S split into N contiguous chunks, one per rank, one tree of S built
+cooperatively (digit all-gather, all-to-all over NCCL), complete on every
+rank; value = n*L / max-over-ranks time, scaling "strong".
 
 --impl reference times the CPU oracle (oracle/, single-threaded C, the
 paper's serialWT analogue) on a bounded sample of the same workload.
@@ -165,6 +168,7 @@ def main():
     ap.add_argument("--cpu-sample-log2", type=int, default=25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="cooperative sharded build (strong scaling)")
     args = ap.parse_args()
 
     import gen
@@ -217,6 +221,9 @@ def main():
     def barrier():
         if world > 1:
             dist.barrier()
+
+    if args.sharded:
+        return bench_sharded(args, cfg, workload, rank, world, local_rank, dist, wt)
 
     # input: the config stream (rank r of a replica run uses seed + r)
     if world > 1 and rank > 0:
@@ -332,6 +339,66 @@ def main():
     print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_sharded(args, cfg, workload, rank, world, local_rank, dist, wt):
+    """--sharded: one tree of the config's S built by all ranks together."""
+    import torch
+    from paper_1407_8142_b200 import dist as wdist
+    S_host = gen_config(cfg)
+    lo, hi = cfg.n * rank // world, cfg.n * (rank + 1) // world
+    S_dev = torch.from_numpy(S_host[lo:hi].copy()).cuda()
+    del S_host
+    comm = wdist.TorchComm() if world > 1 else _SoloComm()
+    for _ in range(args.warmup):
+        wdist.build_sharded(S_dev, cfg.sigma, comm).free()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    sampler = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            wdist.build_sharded(S_dev, cfg.sigma, comm).free()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms, value = aggregate(e0.elapsed_time(e1) / args.steps, cfg.n * cfg.levels // world, world,
+                          dist if world > 1 else None, torch.device("cuda"))
+    if rank == 0:
+        workload = dict(workload, parallelism=f"shard{world}")
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32" if cfg.elem_bytes == 4 else "u8", "data": "synthetic",
+            "config": workload, "mode": "sharded", "clocks": sampler.summary(),
+            "gpu": torch.cuda.get_device_name(local_rank)}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def gen_config(cfg):
+    import gen
+    return gen.config_input(cfg)
+
+
+class _SoloComm:
+    """World size 1 without a process group (the collectives are identities)."""
+    rank, world = 0, 1
+
+    def all_gather(self, t):
+        return [t.clone()]
+
+    def all_gather_v(self, t):
+        return [t.clone()]
+
+    def all_to_all_v(self, t, send_counts):
+        return t.clone()
 
 
 if __name__ == "__main__":

@@ -265,6 +265,44 @@ int hwt_access(const hwt_tree *t, const uint64_t *d_pos, uint64_t q, uint32_t *d
 int hwt_rank(const hwt_tree *t, const uint32_t *d_sym, const uint64_t *d_pos, uint64_t q,
              uint64_t *d_out, void *stream);
 
+/* ---- sharded build helpers (orchestrated by the Python
+ * module paper_1407_8142_b200/dist.py over torch.distributed / NCCL) ----
+ *
+ * With S split into contiguous chunks, one per GPU, levels 0..tau-1 of the
+ * tree are runs of each chunk placed at global offsets, and levels >= tau
+ * are built by the owner of each top-tau digit range from S_tau restricted
+ * to that range (S_tau = S stably sorted by its top tau bits, PAPER.md:
+ * 468-475); see DESIGN.md §8.
+ *
+ * wt_digit_counts -- d_counts[d] (DEVICE u64[2^tau]) = number of i with
+ *   ((S[i] >> shift) & (2^tau - 1)) == d, 1 <= tau <= 8.  Validates
+ *   S[i] < sigma (WT_ESYMBOL).  Synchronises `stream` once.
+ * wt_digits -- d_out[i] (DEVICE u8) = (S[i] >> shift) & (2^tau - 1).  Async.
+ * wt_partition -- d_out (DEVICE, n symbols of elem_bytes, caller-owned,
+ *   must not alias d_in) = d_in stably sorted by ((x >> shift) & (2^tau-1)).
+ *   Asynchronous on `stream`.
+ * wt_gather_bits -- DEVICE u64 d_dst[0, dst_words) = bits gathered from the
+ *   LSB-first bit array d_src by nseg segments d_segs[3k..3k+2] = (dst_bit,
+ *   src_bit, len) (DEVICE u64), sorted by dst_bit and disjoint; bits no
+ *   segment covers are 0.  Asynchronous.
+ * wt_create -- allocate a wt_tree for n symbols over sigma with total_nodes
+ *   node entries; bits are zeroed, every other array is left for the caller
+ *   to fill through its device pointers (level_node_ptr, node_key,
+ *   node_start), then wt_finish computes the rank directory from the bits
+ *   and synchronises.  Released by wt_free.  Errors as wt_build.
+ */
+int wt_digit_counts(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma, uint32_t shift,
+                    uint32_t tau, uint64_t *d_counts, void *stream);
+int wt_digits(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint32_t shift, uint32_t tau, uint8_t *d_out,
+              void *stream);
+int wt_partition(const void *d_in, uint64_t n, uint32_t elem_bytes, uint32_t shift, uint32_t tau, void *d_out,
+                 void *stream);
+int wt_gather_bits(const uint64_t *d_src, const uint64_t *d_segs, uint64_t nseg, uint64_t *d_dst,
+                   uint64_t dst_words, void *stream);
+int wt_create(uint64_t n, uint64_t sigma, uint32_t elem_bytes, uint64_t total_nodes, void *stream,
+              wt_tree **out);
+int wt_finish(wt_tree *t, void *stream);
+
 /* ---- measurement hooks (used by bench.py; no effect on results) ---- */
 
 #define WT_PROF_MAX 32

@@ -563,3 +563,89 @@ def hwt_build(seq: torch.Tensor, sigma: int, stream=None) -> HuffmanWaveletTree:
     if rc != WT_OK:
         raise WtError(rc, "hwt_build")
     return HuffmanWaveletTree(out, seq.device)
+
+
+# ------------------------------------------------ sharded-build helpers (C ABI)
+def _load_dist():
+    lib = _load()
+    if getattr(lib, "_dist_ready", False):
+        return lib
+    V, U64, U32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
+    lib.wt_digit_counts.argtypes = [V, U64, U32, U64, U32, U32, V, V]
+    lib.wt_digits.argtypes = [V, U64, U32, U32, U32, V, V]
+    lib.wt_partition.argtypes = [V, U64, U32, U32, U32, V, V]
+    lib.wt_gather_bits.argtypes = [V, V, U64, V, U64, V]
+    lib.wt_create.argtypes = [U64, U64, U32, U64, V, ctypes.POINTER(ctypes.POINTER(_WtTree))]
+    lib.wt_finish.argtypes = [ctypes.POINTER(_WtTree), V]
+    for f in ("wt_digit_counts", "wt_digits", "wt_partition", "wt_gather_bits", "wt_create", "wt_finish"):
+        getattr(lib, f).restype = ctypes.c_int
+    lib._dist_ready = True
+    return lib
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr() if t.numel() else 0)
+
+
+def digit_counts(seq: torch.Tensor, sigma: int, shift: int, tau: int, stream=None) -> torch.Tensor:
+    """wt_digit_counts: u64 counts of the tau-bit digit (seq >> shift); raises WT_ESYMBOL."""
+    lib = _load_dist()
+    seq = seq.contiguous().view(-1)
+    out = torch.empty(1 << tau, dtype=torch.int64, device=seq.device)
+    rc = lib.wt_digit_counts(_ptr(seq), seq.numel(), _elem_bytes(seq), int(sigma), shift, tau, _ptr(out),
+                             ctypes.c_void_p(_stream_ptr(stream)))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_digit_counts")
+    return out
+
+
+def digits(seq: torch.Tensor, shift: int, tau: int, stream=None) -> torch.Tensor:
+    """wt_digits: u8 tensor of (seq >> shift) & (2^tau - 1)."""
+    lib = _load_dist()
+    seq = seq.contiguous().view(-1)
+    out = torch.empty(seq.numel(), dtype=torch.uint8, device=seq.device)
+    rc = lib.wt_digits(_ptr(seq), seq.numel(), _elem_bytes(seq), shift, tau, _ptr(out),
+                       ctypes.c_void_p(_stream_ptr(stream)))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_digits")
+    return out
+
+
+def partition(seq: torch.Tensor, shift: int, tau: int, stream=None) -> torch.Tensor:
+    """wt_partition: seq stably sorted by its tau-bit digit at `shift`."""
+    lib = _load_dist()
+    seq = seq.contiguous().view(-1)
+    out = torch.empty_like(seq)
+    rc = lib.wt_partition(_ptr(seq), seq.numel(), _elem_bytes(seq), shift, tau, _ptr(out),
+                          ctypes.c_void_p(_stream_ptr(stream)))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_partition")
+    return out
+
+
+def gather_bits(src: torch.Tensor, segs: torch.Tensor, dst: torch.Tensor, stream=None) -> None:
+    """wt_gather_bits: dst (u64 words) <- bit segments (dst_bit, src_bit, len) of src."""
+    lib = _load_dist()
+    segs = segs.contiguous().view(-1)
+    rc = lib.wt_gather_bits(_ptr(src), _ptr(segs), segs.numel() // 3, _ptr(dst), dst.numel(),
+                            ctypes.c_void_p(_stream_ptr(stream)))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_gather_bits")
+
+
+def create(n: int, sigma: int, elem_bytes: int, total_nodes: int, device, stream=None) -> WaveletTree:
+    """wt_create: an empty library-owned tree to be filled, then finish()."""
+    lib = _load_dist()
+    out = ctypes.POINTER(_WtTree)()
+    rc = lib.wt_create(int(n), int(sigma), int(elem_bytes), int(total_nodes), ctypes.c_void_p(_stream_ptr(stream)),
+                       ctypes.byref(out))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_create")
+    return WaveletTree(out, device)
+
+
+def finish(tree: WaveletTree, stream=None) -> None:
+    """wt_finish: rank directory from the tree's bits (synchronises)."""
+    rc = _load_dist().wt_finish(tree.handle, ctypes.c_void_p(_stream_ptr(stream)))
+    if rc != WT_OK:
+        raise WtError(rc, "wt_finish")
