@@ -193,8 +193,8 @@ GroupLaunch group_launch() {
 struct LocalLaunch {
   void (*count)(LocalParams) = nullptr;
   void (*build)(LocalParams) = nullptr;
-  size_t smem = 0;
-  int grid = 0;
+  size_t smem = 0, smem_count = 0;
+  int grid = 0, grid_count = 0;
 };
 
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
@@ -204,12 +204,16 @@ LocalLaunch local_launch() {
   std::call_once(f, [] {
     ll.count = k_local<InT, RecT, OutT, HAS_OUT, true>;
     ll.build = k_local<InT, RecT, OutT, HAS_OUT, false>;
-    ll.smem = LOCAL_WARPS * sizeof(LocalSmem<RecT>);
-    cudaFuncSetAttribute(ll.count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem);
+    ll.smem = LOCAL_WARPS * sizeof(LocalSmem<RecT, false>);
+    ll.smem_count = LOCAL_WARPS * sizeof(LocalSmem<RecT, true>);
+    cudaFuncSetAttribute(ll.count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem_count);
     cudaFuncSetAttribute(ll.build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ll.build, LOCAL_WARPS * 32, ll.smem);
     ll.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
+    per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ll.count, LOCAL_WARPS * 32, ll.smem_count);
+    ll.grid_count = num_sms() * (per_sm < 1 ? 1 : per_sm);
   });
   return ll;
 }
@@ -511,7 +515,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       if (gb.nk) {
         // A4 pass 1: node counts per batch and level, then their scan (CSR offsets)
         rec.begin("k_local_count", n * gb.inw);
-        gb.ll.count<<<gb.ll.grid, LOCAL_WARPS * 32, gb.ll.smem, s>>>(lp);
+        gb.ll.count<<<gb.ll.grid_count, LOCAL_WARPS * 32, gb.ll.smem_count, s>>>(lp);
         chk(cudaGetLastError());
         k_scan_rows_1<<<dim3(gb.nblk, gb.nk), 1024, 0, s>>>(gb.rowcnt, gb.nbatch, gb.bcounts, gb.bsum, gb.nblk, err);
         k_scan_rows_2<<<gb.nk, 1024, 0, s>>>(gb.bsum, gb.nblk, gb.bcounts, gb.l0, gb.k_lo, gb.nk, L, ncount,

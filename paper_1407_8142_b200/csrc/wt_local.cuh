@@ -18,6 +18,9 @@
 //    (the stable order of Fig. 1 / PAPER.md:468-475), maintained with two lane
 //    masks (lt: smaller prefix, eq: same prefix) updated by one ballot per
 //    level; the level's bits are one warp OR-reduction of (bit << pos_k).
+//  * 33..64 symbols: the same with two symbols per lane and 64-bit masks
+//    (config 5: ~45 % of the level-24 nodes).  The next row's start, key and
+//    first 64 symbols are loaded while the current row is processed.
 //  * larger rows: the tile path of k_group (shared-memory stable splits with
 //    the row's split tables), bits copied into the batch staging.
 // Node tables (A4): pass 1 (COUNT) counts each batch's nodes per level; after
@@ -47,11 +50,12 @@ struct LocalParams {
   uint32_t *err;
 };
 
-template <typename RecT>
+// Per-warp shared memory; the counting pass needs no records, staging or level bits.
+template <typename RecT, bool COUNT>
 struct LocalSmem {
-  alignas(16) RecT buf[2][TW];
-  alignas(16) uint32_t SB[TAU_MAX][2 * NCH + 2];  // batch staging bitmaps (<= 2*TW bits)
-  alignas(16) uint32_t LB[NCH];
+  alignas(16) RecT buf[2][COUNT ? 1 : TW];
+  alignas(16) uint32_t SB[TAU_MAX][COUNT ? 1 : 2 * NCH + 2];  // batch staging bitmaps (<= 2*TW bits)
+  alignas(16) uint32_t LB[COUNT ? 1 : NCH];
   uint32_t hist2[NDIG / 2];
   uint16_t Hl[NDIG + 2];
   uint16_t T[NDIG];
@@ -70,7 +74,8 @@ template <typename InT, typename RecT, typename OutT, bool HAS_OUT, bool COUNT>
 __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  LocalSmem<RecT> &ws = *reinterpret_cast<LocalSmem<RecT> *>(smem_raw + warp * sizeof(LocalSmem<RecT>));
+  LocalSmem<RecT, COUNT> &ws =
+      *reinterpret_cast<LocalSmem<RecT, COUNT> *>(smem_raw + warp * sizeof(LocalSmem<RecT, COUNT>));
   if (ld_relaxed(p.err)) return;
   const InT *keys = reinterpret_cast<const InT *>(p.keys_in);
   OutT *ko = reinterpret_cast<OutT *>(p.keys_out);
@@ -105,16 +110,25 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
     if (lane < (int)p.nk) nodeoff = COUNT ? 0u : p.batchcnt[(uint64_t)lane * p.nbatch + b];
     __syncwarp();
 
+    // the next row's start, key and first 64 symbols are loaded one row ahead
+    uint32_t rs_n = A, re_n = r0 + 1 < nrows ? p.row_start[r0 + 1] : (uint32_t)p.n, P_n = p.row_key[r0];
+    uint32_t kA_n = rs_n + lane < p.n ? (uint32_t)keys[rs_n + lane] : 0u;
+    uint32_t kB_n = rs_n + 32 + lane < p.n ? (uint32_t)keys[rs_n + 32 + lane] : 0u;
     for (uint32_t r = r0; r < r1; r++) {
-      const uint32_t rs = p.row_start[r];
-      const uint32_t re = r + 1 < nrows ? p.row_start[r + 1] : (uint32_t)p.n;
+      const uint32_t rs = rs_n, re = re_n, P = P_n, kA0 = kA_n, kB0 = kB_n;
       const uint32_t len = re - rs;
-      const uint32_t P = p.row_key[r];
+      if (r + 1 < r1) {
+        rs_n = re;
+        re_n = r + 2 < nrows ? p.row_start[r + 2] : (uint32_t)p.n;
+        P_n = p.row_key[r + 1];
+        kA_n = rs_n + lane < p.n ? (uint32_t)keys[rs_n + lane] : 0u;
+        kB_n = rs_n + 32 + lane < p.n ? (uint32_t)keys[rs_n + 32 + lane] : 0u;
+      }
       const uint32_t soff = rs - A;  // the row's bit offset inside the batch staging
       if (len <= 32) {
         // ---------------- register path ----------------
         const bool valid = (uint32_t)lane < len;
-        const uint32_t key = valid ? (uint32_t)keys[rs + lane] : 0u;
+        const uint32_t key = valid ? kA0 : 0u;
         const uint32_t dig = (key >> pbits) & (ndig - 1u);
         uint32_t eq = __ballot_sync(FULL, valid), ltm = 0;  // same prefix / smaller prefix (this row)
         for (uint32_t k = 0; k < tau; k++) {
@@ -147,6 +161,59 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
         if (HAS_OUT && !COUNT && valid) ko[rs + __popc(ltm) + __popc(eq & lt)] = (OutT)(key & pmask);
         continue;
       }
+      if (len <= 64) {
+        // ---------------- register path, two symbols per lane ----------------
+        // symbols x = lane (A) and x = 32 + lane (B); 64-bit masks over the row:
+        // eq = same prefix as x, ltm = smaller prefix than x, before = index < x.
+        const bool vA = true, vB = (uint32_t)lane + 32u < len;
+        const uint32_t kA = kA0;
+        const uint32_t kB = vB ? kB0 : 0u;
+        const uint32_t dA = (kA >> pbits) & (ndig - 1u), dB = (kB >> pbits) & (ndig - 1u);
+        const uint64_t valid64 = ((uint64_t)__ballot_sync(FULL, vB) << 32) | 0xffffffffull;
+        const uint64_t befA = (uint64_t)lt, befB = 0xffffffffull | ((uint64_t)lt << 32);
+        uint64_t eqA = valid64, eqB = valid64, ltA = 0, ltB = 0;
+        for (uint32_t k = 0; k < tau; k++) {
+          const uint32_t bA = (dA >> (tau - 1u - k)) & 1u, bB = (dB >> (tau - 1u - k)) & 1u;
+          const uint64_t M = ((uint64_t)__ballot_sync(FULL, vB && bB) << 32) | __ballot_sync(FULL, vA && bA);
+          if (!COUNT) {
+            const uint32_t pA = __popcll(ltA) + __popcll(eqA & befA);
+            const uint32_t pB = __popcll(ltB) + __popcll(eqB & befB);
+            uint32_t lo = 0, hi = 0;
+            if (bA) { if (pA < 32) lo |= 1u << pA; else hi |= 1u << (pA - 32); }
+            if (vB && bB) { if (pB < 32) lo |= 1u << pB; else hi |= 1u << (pB - 32); }
+            lo = __reduce_or_sync(FULL, lo);
+            hi = __reduce_or_sync(FULL, hi);
+            if (lane == 0) {
+              stage_bits(ws.SB[k], soff, lo);
+              stage_bits(ws.SB[k], soff + 32, hi);
+            }
+          }
+          if (bA) { ltA |= eqA & ~M; eqA &= M; } else { eqA &= ~M; }
+          if (bB) { ltB |= eqB & ~M; eqB &= M; } else { eqB &= ~M; }
+          if (k + 1 <= p.nk) {  // nodes of level l0+k+1 = distinct (k+1)-bit prefixes
+            const bool fA = (eqA & befA) == 0, fB = vB && (eqB & befB) == 0;
+            const uint64_t F = ((uint64_t)__ballot_sync(FULL, fB) << 32) | __ballot_sync(FULL, fA);
+            const uint32_t base = __shfl_sync(FULL, nodeoff, k);
+            if (!COUNT) {
+              const uint64_t j0 = p.level_node_ptr[p.l0 + k + 1] + base;
+              if (fA) {
+                p.node_key[j0 + __popcll(F & ltA)] = (P << (k + 1)) | (dA >> (tau - 1u - k));
+                p.node_start[j0 + __popcll(F & ltA)] = rs + __popcll(ltA);
+              }
+              if (fB) {
+                p.node_key[j0 + __popcll(F & ltB)] = (P << (k + 1)) | (dB >> (tau - 1u - k));
+                p.node_start[j0 + __popcll(F & ltB)] = rs + __popcll(ltB);
+              }
+            }
+            if (lane == (int)k) nodeoff += __popcll(F);
+          }
+        }
+        if (HAS_OUT && !COUNT) {
+          ko[rs + __popcll(ltA) + __popcll(eqA & befA)] = (OutT)(kA & pmask);
+          if (vB) ko[rs + __popcll(ltB) + __popcll(eqB & befB)] = (OutT)(kB & pmask);
+        }
+        continue;
+      }
       // ---------------- tile path (32 < len <= TW) ----------------
       if (len > (uint32_t)TW) {
         if (lane == 0) atomicOr(p.err, 2u);
@@ -158,7 +225,7 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
       for (uint32_t pos = lane; pos < len; pos += 32) {
         const uint32_t key = (uint32_t)keys[rs + pos];
         const uint32_t dig = (key >> pbits) & (ndig - 1u);
-        ws.buf[0][pos] = (RecT)((dig << pbits) | (key & pmask));
+        if constexpr (!COUNT) ws.buf[0][pos] = (RecT)((dig << pbits) | (key & pmask));
         atomicAdd(&ws.hist2[dig >> 1], 1u << ((dig & 1u) << 4));
       }
       __syncwarp();

@@ -218,3 +218,21 @@ def test_full_config5_vs_oracle():
             assert np.array_equal(got, want), f"{k} differs"
             del want, got
         tree.free()
+
+
+# ---- local mode, rows of 33..64 symbols (two symbols per lane) and their edges ----
+@pytest.mark.parametrize("n,sigma", [(12288, 1 << 16), (20000, 1 << 12), (3 << 20, 1 << 24), (9000, 1 << 20)])
+def test_local_rows_pair_path(n, sigma):
+    S = gen.uniform_below(n, sigma, seed=n ^ sigma, dtype=np.uint32)
+    _compare(S, sigma)
+
+
+@pytest.mark.parametrize("sizes", [(33, 64, 65, 32, 1, 48), (64,) * 40, (40, 63, 33, 2, 64, 31, 64)])
+def test_local_rows_exact_sizes(sizes):
+    # level-8 nodes of chosen sizes (sigma = 2^16: group 1 runs in local mode)
+    rng = np.random.default_rng(len(sizes))
+    parts = [(np.uint32(p) << np.uint32(8)) | rng.integers(0, 256, s).astype(np.uint32)
+             for p, s in zip(rng.choice(256, len(sizes), replace=False), sizes)]
+    S = np.concatenate(parts)
+    rng.shuffle(S)
+    _compare(S, 1 << 16)
