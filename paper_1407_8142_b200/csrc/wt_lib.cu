@@ -193,8 +193,9 @@ GroupLaunch group_launch() {
 struct LocalLaunch {
   void (*count)(LocalParams) = nullptr;
   void (*build)(LocalParams) = nullptr;
-  size_t smem = 0, smem_count = 0;
-  int grid = 0, grid_count = 0;
+  void (*big)(LocalParams) = nullptr;
+  size_t smem = 0, smem_count = 0, smem_big = 0;
+  int grid = 0, grid_count = 0, grid_big = 0;
 };
 
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
@@ -202,18 +203,21 @@ LocalLaunch local_launch() {
   static LocalLaunch ll;
   static std::once_flag f;
   std::call_once(f, [] {
-    ll.count = k_local<InT, RecT, OutT, HAS_OUT, true>;
-    ll.build = k_local<InT, RecT, OutT, HAS_OUT, false>;
-    ll.smem = LOCAL_WARPS * sizeof(LocalSmem<RecT, false>);
-    ll.smem_count = LOCAL_WARPS * sizeof(LocalSmem<RecT, true>);
-    cudaFuncSetAttribute(ll.count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem_count);
-    cudaFuncSetAttribute(ll.build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ll.build, LOCAL_WARPS * 32, ll.smem);
-    ll.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
-    per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ll.count, LOCAL_WARPS * 32, ll.smem_count);
-    ll.grid_count = num_sms() * (per_sm < 1 ? 1 : per_sm);
+    ll.count = k_local<InT, RecT, OutT, HAS_OUT, LM_COUNT>;
+    ll.build = k_local<InT, RecT, OutT, HAS_OUT, LM_BUILD>;
+    ll.big = k_local<InT, RecT, OutT, HAS_OUT, LM_BIG>;
+    ll.smem_count = LOCAL_WARPS * sizeof(LocalSmem<RecT, LM_COUNT>);
+    ll.smem = LOCAL_WARPS * sizeof(LocalSmem<RecT, LM_BUILD>);
+    ll.smem_big = LOCAL_WARPS * sizeof(LocalSmem<RecT, LM_BIG>);
+    auto setup = [](void (*f)(LocalParams), size_t smem, int *grid) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, LOCAL_WARPS * 32, smem);
+      *grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
+    };
+    setup(ll.count, ll.smem_count, &ll.grid_count);
+    setup(ll.build, ll.smem, &ll.grid);
+    setup(ll.big, ll.smem_big, &ll.grid_big);
   });
   return ll;
 }
@@ -266,7 +270,9 @@ struct GroupBufs {
   GroupLaunch gl;
   LocalLaunch ll;
   uint32_t nbatch = 0;
-  uint32_t *batch_first = nullptr, *bcounts = nullptr;
+  uint32_t *batch_first = nullptr, *bcounts = nullptr;  // bcounts: [0] claim counter, [1] batches, [2] deferred rows
+  uint64_t ndefer = 0;
+  uint32_t *defer = nullptr;
   void *keys_out = nullptr;
   uint32_t *chain_begin = nullptr, *chain_end = nullptr, *chain_row = nullptr;
   uint32_t *row_first = nullptr, *row_start = nullptr, *row_key = nullptr;
@@ -294,6 +300,7 @@ struct GroupBufs {
     if (local) {
       batch_first = A.alloc<uint32_t>(nbatch + 1, false);
       bcounts = A.alloc<uint32_t>(4, false);
+      defer = A.alloc<uint32_t>(ndefer * DEFER_W, false);
     }
     counts = A.alloc<uint32_t>(4, false);
   }
@@ -381,6 +388,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     }
     if (gb.local) {
       gb.nbatch = (uint32_t)((n + TW - 1) / TW);
+      gb.ndefer = n / (LT + 1) + 1;
       gb.max_chains = 1;
     } else {
       const uint64_t warps = (uint64_t)gb.gl.grid;  // CTAs (one chain at a time each)
@@ -512,6 +520,9 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       lp.bits = t->bits;
       lp.wpl = WPL;
       lp.err = err;
+      lp.defer = gb.defer;
+      lp.defer_count = gb.bcounts + 2;
+      chk(cudaMemsetAsync(gb.bcounts + 2, 0, sizeof(uint32_t), s));
       if (gb.nk) {
         // A4 pass 1: node counts per batch and level, then their scan (CSR offsets)
         rec.begin("k_local_count", n * gb.inw);
@@ -531,6 +542,9 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       snprintf(name, sizeof(name), "k_group%u", g);
       rec.begin(name, n * gb.inw + (has_out ? n * gb.outw : 0) + (uint64_t)gb.tau * n / 8);
       gb.ll.build<<<gb.ll.grid, LOCAL_WARPS * 32, gb.ll.smem, s>>>(lp);
+      chk(cudaGetLastError());
+      chk(cudaMemsetAsync(gb.bcounts, 0, sizeof(uint32_t), s));  // claim counter for the deferred rows
+      gb.ll.big<<<gb.ll.grid_big, LOCAL_WARPS * 32, gb.ll.smem_big, s>>>(lp);
       chk(cudaGetLastError());
       rec.end();
       rank_levels(gb.l0, gb.tau);

@@ -23,8 +23,10 @@
 //    first 64 symbols are loaded while the current row is processed.
 //  * larger rows: the tile path of k_group (shared-memory stable splits with
 //    the row's split tables), bits copied into the batch staging.
-// Node tables (A4): pass 1 (COUNT) counts each batch's nodes per level; after
-// a scan over batches, pass 2 writes them in (level, row, prefix) order.
+// Node tables (A4): pass 1 (LM_COUNT) counts each batch's nodes per level;
+// after a scan over batches, pass 2 (LM_BUILD) writes them in (level, row,
+// prefix) order, and pass 3 (LM_BIG) finishes the rows longer than LT that
+// pass 2 deferred (their node offsets recorded, their bits OR-ed in).
 #pragma once
 #include "wt_common.cuh"
 
@@ -48,14 +50,26 @@ struct LocalParams {
   uint64_t *bits;
   uint64_t wpl;
   uint32_t *err;
+  uint32_t *defer;        // rows longer than LT left by the build pass: [row, nodeoff x 8] each
+  uint32_t *defer_count;  // entries in defer
 };
 
+// Passes of the local mode: node counts, the build of every row up to LT
+// symbols, and the build of the longer rows the build pass deferred (one
+// "batch" per such row).  Splitting off the rare long rows keeps the build
+// pass's per-warp shared memory small (occupancy: it is latency-bound).
+enum : int { LM_COUNT = 0, LM_BUILD = 1, LM_BIG = 2 };
+constexpr uint32_t LT = 1024;
+constexpr uint32_t DEFER_W = 1 + TAU_MAX;  // u32 per deferred row
+
 // Per-warp shared memory; the counting pass needs no records, staging or level bits.
-template <typename RecT, bool COUNT>
+template <typename RecT, int MODE>
 struct LocalSmem {
-  alignas(16) RecT buf[2][COUNT ? 1 : TW];
-  alignas(16) uint32_t SB[TAU_MAX][COUNT ? 1 : 2 * NCH + 2];  // batch staging bitmaps (<= 2*TW bits)
-  alignas(16) uint32_t LB[COUNT ? 1 : NCH];
+  static constexpr uint32_t BUFN = MODE == LM_COUNT ? 1 : (MODE == LM_BUILD ? LT : TW);
+  static constexpr uint32_t SBW = MODE == LM_COUNT ? 1 : (MODE == LM_BUILD ? 2 * NCH + 2 : NCH + 2);
+  alignas(16) RecT buf[2][BUFN];
+  alignas(16) uint32_t SB[TAU_MAX][SBW];  // batch staging bitmaps
+  alignas(16) uint32_t LB[MODE == LM_COUNT ? 1 : BUFN / 32];
   uint32_t hist2[NDIG / 2];
   uint16_t Hl[NDIG + 2];
   uint16_t T[NDIG];
@@ -70,12 +84,13 @@ __device__ __forceinline__ void stage_bits(uint32_t *SB, uint32_t off, uint32_t 
   if (sh) SB[w + 1] |= v >> (32 - sh);
 }
 
-template <typename InT, typename RecT, typename OutT, bool HAS_OUT, bool COUNT>
+template <typename InT, typename RecT, typename OutT, bool HAS_OUT, int MODE>
 __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
+  constexpr bool COUNT = MODE == LM_COUNT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  LocalSmem<RecT, COUNT> &ws =
-      *reinterpret_cast<LocalSmem<RecT, COUNT> *>(smem_raw + warp * sizeof(LocalSmem<RecT, COUNT>));
+  LocalSmem<RecT, MODE> &ws =
+      *reinterpret_cast<LocalSmem<RecT, MODE> *>(smem_raw + warp * sizeof(LocalSmem<RecT, MODE>));
   if (ld_relaxed(p.err)) return;
   const InT *keys = reinterpret_cast<const InT *>(p.keys_in);
   OutT *ko = reinterpret_cast<OutT *>(p.keys_out);
@@ -88,8 +103,10 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
     uint32_t b = 0;
     if (lane == 0) b = atomicAdd(p.batch_counter, 1u);
     b = __shfl_sync(FULL, b, 0);
-    if (b >= p.nbatch) break;
-    const uint32_t r0 = p.batch_first[b], r1 = p.batch_first[b + 1];
+    const uint32_t nb = MODE == LM_BIG ? ld_relaxed(p.defer_count) : p.nbatch;
+    if (b >= nb) break;
+    const uint32_t r0 = MODE == LM_BIG ? p.defer[(uint64_t)b * DEFER_W] : p.batch_first[b];
+    const uint32_t r1 = MODE == LM_BIG ? r0 + 1 : p.batch_first[b + 1];
     if (r0 >= r1) {  // no row starts in this window: it contributes no nodes
       if (COUNT && lane < (int)p.nk) p.batchcnt[(uint64_t)lane * p.nbatch + b] = 0;
       continue;
@@ -107,7 +124,9 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
     }
     // running node offsets (lane kk holds level l0+1+kk), from the batch scan
     uint32_t nodeoff = 0;
-    if (lane < (int)p.nk) nodeoff = COUNT ? 0u : p.batchcnt[(uint64_t)lane * p.nbatch + b];
+    if (lane < (int)p.nk)
+      nodeoff = COUNT ? 0u : (MODE == LM_BIG ? p.defer[(uint64_t)b * DEFER_W + 1 + lane]
+                                             : p.batchcnt[(uint64_t)lane * p.nbatch + b]);
     __syncwarp();
 
     // the next row's start, key and first 64 symbols are loaded one row ahead
@@ -214,10 +233,21 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
         }
         continue;
       }
-      // ---------------- tile path (32 < len <= TW) ----------------
+      // ---------------- tile path (64 < len <= TW) ----------------
       if (len > (uint32_t)TW) {
         if (lane == 0) atomicOr(p.err, 2u);
         break;
+      }
+      // the build pass leaves rows longer than its buffers to the LM_BIG pass:
+      // record where their nodes go, count them, emit nothing
+      bool emit = !COUNT;
+      if (MODE == LM_BUILD && len > LT) {
+        uint32_t e = 0;
+        if (lane == 0) e = atomicAdd(p.defer_count, 1u);
+        e = __shfl_sync(FULL, e, 0);
+        if (lane == 0) p.defer[(uint64_t)e * DEFER_W] = r;
+        if (lane < (int)p.nk) p.defer[(uint64_t)e * DEFER_W + 1 + lane] = nodeoff;
+        emit = false;
       }
       const uint32_t nch = (len + 31) >> 5;
       for (uint32_t d = lane; d < NDIG / 2; d += 32) ws.hist2[d] = 0;
@@ -225,7 +255,7 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
       for (uint32_t pos = lane; pos < len; pos += 32) {
         const uint32_t key = (uint32_t)keys[rs + pos];
         const uint32_t dig = (key >> pbits) & (ndig - 1u);
-        if constexpr (!COUNT) ws.buf[0][pos] = (RecT)((dig << pbits) | (key & pmask));
+        if (!COUNT && emit) ws.buf[0][pos] = (RecT)((dig << pbits) | (key & pmask));
         atomicAdd(&ws.hist2[dig >> 1], 1u << ((dig & 1u) << 4));
       }
       __syncwarp();
@@ -251,7 +281,7 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
           const uint32_t q = q0 + lane;
           const bool ne = q < nq && ws.Hl[(q + 1) << sh] > ws.Hl[q << sh];
           const uint32_t bm = __ballot_sync(FULL, ne);
-          if (!COUNT && ne) {
+          if (emit && ne) {
             const uint64_t j = p.level_node_ptr[p.l0 + k] + base + __popc(bm & lt);
             p.node_key[j] = (P << k) | q;
             p.node_start[j] = rs + ws.Hl[q << sh];
@@ -260,7 +290,7 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
         }
         if (lane == (int)(k - 1)) nodeoff = base;
       }
-      if constexpr (!COUNT) {
+      if (!COUNT && emit) {
       for (uint32_t k = 0; k < tau; k++) {
         const uint32_t nq = 1u << k, sh = tau - k;
         const bool do_split = HAS_OUT || (k + 1 < tau);

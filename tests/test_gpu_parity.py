@@ -227,7 +227,9 @@ def test_local_rows_pair_path(n, sigma):
     _compare(S, sigma)
 
 
-@pytest.mark.parametrize("sizes", [(33, 64, 65, 32, 1, 48), (64,) * 40, (40, 63, 33, 2, 64, 31, 64)])
+@pytest.mark.parametrize("sizes", [(33, 64, 65, 32, 1, 48), (64,) * 40, (40, 63, 33, 2, 64, 31, 64),
+                                   (4096, 2000, 1025, 1024, 1100, 70, 65, 64, 33, 1) + (10,) * 200,
+                                   (1025,) * 3 + (7,) * 100])
 def test_local_rows_exact_sizes(sizes):
     # level-8 nodes of chosen sizes (sigma = 2^16: group 1 runs in local mode)
     rng = np.random.default_rng(len(sizes))
