@@ -263,9 +263,11 @@ __device__ __forceinline__ uint32_t split_range(const uint16_t *T, const uint16_
   constexpr uint32_t RB = sizeof(RecT);
   uint32_t bitmask = 1u << bitsh;
   asm("" : "+r"(bitmask));  // opaque: test the bit with one LOP3 instead of shift+mask+compare
-  const uint32_t TA = smem_u32(T);
-  const uint32_t LA = smem_u32(LB);
-  const uint32_t sA = srcA + (A + lane) * RB;
+  // opaque copies: keep these in registers instead of recomputing them from
+  // special registers / kernel parameters inside the loop
+  uint32_t TA = smem_u32(T), LA = smem_u32(LB), Al = A + lane;
+  asm("" : "+r"(TA), "+r"(LA), "+r"(Al), "+r"(bitsh));
+  const uint32_t sA = srcA + Al * RB;
   uint32_t Orun = Obase;
   const uint32_t full = wl / (32 * U);
   for (uint32_t b = 0; b < full; b++) {
@@ -275,7 +277,7 @@ __device__ __forceinline__ uint32_t split_range(const uint16_t *T, const uint16_
     for (int u = 0; u < U; u++) r[u] = lds<RecT>(sA + (cb + u * 32) * RB);
     if constexpr (DO_SPLIT) {
       const uint32_t fq = FB[b];
-      const uint32_t pb = A + cb + lane;
+      const uint32_t pb = Al + cb;
       if (fq != FB_NONE) {  // one class: uniform destinations
         const uint32_t a01 = lds<uint32_t>(TA + 4 * fq);
         const uint32_t a0 = __byte_perm(a01, 0, 0x4410), a1 = __byte_perm(a01, 0, 0x4432);
