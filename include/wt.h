@@ -241,7 +241,7 @@ typedef struct hwt_tree {
   uint32_t *code;             /* u32[sigma] canonical code (right-aligned)    */
   uint8_t *code_len;          /* u8[sigma], 0 = symbol absent                 */
   uint32_t only_symbol;       /* levels == 0 && n > 0: the single symbol      */
-  uint32_t pad_;
+  uint32_t stages;            /* padded-code passes used by the build (diagnostic) */
   uint64_t total_bits;        /* sum of level_len                             */
   void *internal;             /* library bookkeeping; do not touch            */
 } hwt_tree;

@@ -464,9 +464,9 @@ __global__ void __launch_bounds__(1024) k_hwt_segments(const uint64_t *__restric
                                                        const HuffCanon *__restrict__ canon, const uint64_t *__restrict__ info,
                                                        uint32_t *__restrict__ seg_src, uint32_t *__restrict__ seg_dst,
                                                        uint32_t *__restrict__ seg_key, uint32_t *__restrict__ alive,
-                                                       uint32_t *err) {
+                                                       uint32_t *err, uint32_t lbase) {
   __shared__ uint32_t shm[33];
-  const uint32_t l = blockIdx.x;
+  const uint32_t l = lbase + blockIdx.x;
   const uint64_t lo = pptr[l], hi = pptr[l + 1];
   uint32_t nalive = 0, dst = 0;
   for (uint64_t j0 = lo; j0 < hi; j0 += blockDim.x) {
@@ -501,9 +501,68 @@ __global__ void __launch_bounds__(1024) k_hwt_segments(const uint64_t *__restric
   }
 }
 
+// ---------------------------------------------------------------------------
+// Staged mode (skewed codes): the keys of stage g are the padded codes,
+// truncated to their top `hi` bits, of the elements whose code is longer than
+// `lo` (they alone reach level lo), in S order -- a stable compaction.
+// k_hwt_alive_count: per tile of PART_TILE elements, the number alive.
+// k_hwt_alive_scatter: after the scan of the tile counts, each warp ranks its
+// 16 chunks of 32 with ballots.
+// ---------------------------------------------------------------------------
+constexpr uint32_t HA_TILE = 4096, HA_THREADS = 256, HA_PER = HA_TILE / HA_THREADS;
+
+template <typename InT>
+__global__ void __launch_bounds__(HA_THREADS) k_hwt_alive_count(const InT *__restrict__ S, uint64_t n,
+                                                               const uint8_t *__restrict__ code_len, uint32_t lo,
+                                                               uint32_t ntiles, uint32_t *__restrict__ tcount) {
+  __shared__ uint32_t c;
+  if (threadIdx.x == 0) c = 0;
+  __syncthreads();
+  const uint64_t b = (uint64_t)blockIdx.x * HA_TILE;
+  uint32_t mine = 0;
+  for (uint32_t i = threadIdx.x; i < HA_TILE; i += blockDim.x)
+    if (b + i < n && code_len[(uint32_t)S[b + i]] > lo) mine++;
+  mine = __reduce_add_sync(FULL, mine);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&c, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) tcount[blockIdx.x] = c;
+}
+
+template <typename InT, typename OutT>
+__global__ void __launch_bounds__(HA_THREADS) k_hwt_alive_scatter(const InT *__restrict__ S, uint64_t n,
+                                                                 const uint8_t *__restrict__ code_len,
+                                                                 const uint32_t *__restrict__ pad, uint32_t lo,
+                                                                 uint32_t shift, const uint32_t *__restrict__ toff,
+                                                                 OutT *__restrict__ out) {
+  constexpr uint32_t NW = HA_THREADS / 32;
+  __shared__ uint32_t wc[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t wb = (uint64_t)blockIdx.x * HA_TILE + (uint64_t)warp * HA_PER * 32;
+  uint32_t key[HA_PER], m[HA_PER], cnt = 0;
+#pragma unroll
+  for (uint32_t c = 0; c < HA_PER; c++) {
+    const uint64_t j = wb + c * 32 + lane;
+    uint32_t sym = j < n ? (uint32_t)S[j] : 0u;
+    const bool ok = j < n && code_len[sym] > lo;
+    key[c] = ok ? pad[sym] >> shift : 0u;
+    m[c] = __ballot_sync(FULL, ok);
+    cnt += __popc(m[c]);
+  }
+  if (lane == 0) wc[warp] = cnt;
+  __syncthreads();
+  uint32_t off = toff[blockIdx.x];
+  for (int w = 0; w < warp; w++) off += wc[w];
+#pragma unroll
+  for (uint32_t c = 0; c < HA_PER; c++) {
+    if ((m[c] >> lane) & 1u) out[off + __popc(m[c] & lanemask_lt())] = (OutT)key[c];
+    off += __popc(m[c]);
+  }
+}
+
 // Per-level bookkeeping passed by value (host knows it after H2).
 struct HwtLevels {
   uint32_t h;
+  uint32_t lbase;                   // first level of the current stage (blockIdx.y = level - lbase)
   uint64_t nl[HUFF_MAXLEN];
   uint64_t wptr[HUFF_MAXLEN + 1];   // output word offset of each level
   uint64_t segbase[HUFF_MAXLEN];    // padded node-table offset of the level
@@ -524,7 +583,7 @@ __global__ void __launch_bounds__(HB_WORDS) k_hwt_bits(HwtLevels lv, const uint6
                                                        const uint32_t *__restrict__ seg_dst, uint64_t *__restrict__ out) {
   __shared__ uint32_t s_dst[HB_SEGS + 1], s_src[HB_SEGS];
   __shared__ uint32_t s_k0, s_k1;
-  const uint32_t l = blockIdx.y;
+  const uint32_t l = lv.lbase + blockIdx.y;
   const uint64_t nw = lv.wptr[l + 1] - lv.wptr[l];
   const uint64_t w0 = (uint64_t)blockIdx.x * HB_WORDS * HB_WPT;
   if (w0 >= nw) return;
@@ -672,7 +731,7 @@ __global__ void __launch_bounds__(1024) k_hwt_rank_super(HwtRankLv r, const uint
 __global__ void k_hwt_nodes(HwtLevels lv, const uint64_t *__restrict__ optr, const uint32_t *__restrict__ seg_key,
                             const uint32_t *__restrict__ seg_dst, uint32_t *__restrict__ node_key,
                             uint32_t *__restrict__ node_start) {
-  const uint32_t l = blockIdx.y;
+  const uint32_t l = lv.lbase + blockIdx.y;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < lv.nseg[l]; j += gridDim.x * blockDim.x) {
     node_key[optr[l] + j] = seg_key[lv.segbase[l] + j];
     node_start[optr[l] + j] = seg_dst[lv.segbase[l] + j];

@@ -1293,53 +1293,126 @@ int hwt_build_impl(const void *d_seq, uint64_t n, uint32_t eb, uint64_t sigma, v
   chk(cudaMemcpyAsync(t->level_super_ptr, h_sp, (h + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
 
   if (h > 0) {
-    // ---- H3: padded codes ----
-    const uint32_t xw = width_of(h);
-    void *X = A.alloc<uint8_t>(n * xw, false);
-    if (A.fail) return fail(WT_ENOMEM);
-    if (eb == 1) launch_map<uint8_t>(d_seq, n, sg, pad, X, xw, s);
-    else if (eb == 2) launch_map<uint16_t>(d_seq, n, sg, pad, X, xw, s);
-    else launch_map<uint32_t>(d_seq, n, sg, pad, X, xw, s);
-    chk(cudaGetLastError());
-    // ---- H4: balanced levelWT over the padded codes ----
-    wt_tree *pt = nullptr;
-    const int rc = build_impl(X, nullptr, false, n, xw, 1ull << h, stream_v, &pt, false);
-    if (rc != WT_OK) return fail(rc);
-    uint32_t *seg_src = A.alloc<uint32_t>(pt->total_nodes, false);
-    uint32_t *seg_dst = A.alloc<uint32_t>(pt->total_nodes, false);
-    uint32_t *seg_key = A.alloc<uint32_t>(pt->total_nodes, false);
-    uint32_t *alive = A.alloc<uint32_t>(h, false);
-    if (A.fail) { wt_free(pt); return fail(WT_ENOMEM); }
-    k_hwt_segments<<<h, 1024, 0, s>>>(pt->level_node_ptr, pt->node_key, pt->node_start, n, canon, info, seg_src,
-                                      seg_dst, seg_key, alive, err);
-    chk(cudaGetLastError());
-    chk(cudaMemcpyAsync(stage, pt->level_node_ptr, (h + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    chk(cudaMemcpyAsync(stage + 64, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    chk(cudaMemcpyAsync(stage + 128, alive, h * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    chk(cudaStreamSynchronize(s));
-    if (ce != cudaSuccess || (uint32_t)stage[64]) { wt_free(pt); return fail(WT_ECUDA); }
-    const uint32_t *h_alive = reinterpret_cast<const uint32_t *>(stage + 128);
-    uint32_t maxseg = 1;
-    for (uint32_t l = 0; l < h; l++) {
-      lv.segbase[l] = stage[l];
-      lv.nseg[l] = h_alive[l];
-      h_np[l + 1] = h_np[l] + h_alive[l];
-      maxseg = std::max(maxseg, h_alive[l]);
+    // ---- H4: balanced levelWT over the padded codes, in stages ----
+    // Stage [lo, hi) builds the tree of the elements whose code is longer than
+    // lo (the only ones that reach level lo), keyed by the top hi bits of the
+    // padded code, and keeps its levels lo .. hi-1.  One stage [0, h) when
+    // most codes are long; 8-level stages while at least half of the elements
+    // leave the sequence within the stage (skewed codes: work ~ sum of n_lo).
+    // Plan by a cost model in element-group passes: a stage [lo, hi) costs
+    // n_lo * ceil(hi / 8) plus ~0.3 n for its compaction (two reads of S)
+    // unless it is the single stage [0, h); best[lo] = cheapest finish from lo.
+    std::vector<std::pair<uint32_t, uint32_t>> stg;
+    {
+      const uint32_t nb = (h + TAU_MAX - 1) / TAU_MAX;
+      std::vector<double> best(nb + 1, 0.0);
+      std::vector<uint32_t> cut(nb + 1, h);
+      auto nlo = [&](uint32_t lo) { return (double)(lo ? h_len[lo] : n); };
+      for (int bi = (int)nb - 1; bi >= 0; bi--) {
+        const uint32_t lo = (uint32_t)bi * TAU_MAX;
+        const double ov = lo ? 0.3 * (double)n : 0.0;
+        double c = nlo(lo) * nb + ov;  // one stage to the end
+        cut[bi] = h;
+        if (lo + TAU_MAX < h) {
+          const double c2 = nlo(lo) * (bi + 1) + 0.3 * (double)n + best[bi + 1];
+          if (c2 < c) { c = c2; cut[bi] = lo + TAU_MAX; }
+        }
+        best[bi] = c;
+      }
+      for (uint32_t lo = 0; lo < h; lo = cut[lo / TAU_MAX]) stg.push_back({lo, cut[lo / TAU_MAX]});
     }
+    t->stages = (uint32_t)stg.size();
+    // ---- H3: padded codes (single stage; a staged build compacts per stage) ----
+    void *X = nullptr;
+    if (stg.size() == 1) {
+      const uint32_t xw = width_of(h);
+      X = A.alloc<uint8_t>(n * xw, false);
+      if (A.fail) return fail(WT_ENOMEM);
+      if (eb == 1) launch_map<uint8_t>(d_seq, n, sg, pad, X, xw, s);
+      else if (eb == 2) launch_map<uint16_t>(d_seq, n, sg, pad, X, xw, s);
+      else launch_map<uint32_t>(d_seq, n, sg, pad, X, xw, s);
+      chk(cudaGetLastError());
+    }
+    struct StageSegs { uint32_t lo, hi; uint32_t *key, *dst; uint64_t base[HUFF_MAXLEN]; uint32_t cnt[HUFF_MAXLEN]; };
+    std::vector<StageSegs> done;
+    uint32_t maxseg = 1;
+    for (const auto &st : stg) {
+      const uint32_t lo = st.first, hi = st.second;
+      const uint64_t ng = lo ? h_len[lo] : n;
+      const uint32_t kw = width_of(hi);
+      void *Xg = X;
+      if (lo > 0 || hi < h) {  // stage keys: alive elements, top hi bits of the padded code, S order
+        Xg = A.alloc<uint8_t>(ng * kw, false);
+        const uint32_t ntiles = (uint32_t)((n + HA_TILE - 1) / HA_TILE);
+        uint32_t *tc = A.alloc<uint32_t>(ntiles, false);
+        uint64_t *tt = A.alloc<uint64_t>(1, false);
+        if (A.fail) return fail(WT_ENOMEM);
+        auto run = [&](auto in_tag, auto out_tag) {
+          using IT = decltype(in_tag);
+          using OT = decltype(out_tag);
+          k_hwt_alive_count<IT><<<ntiles, HA_THREADS, 0, s>>>((const IT *)d_seq, n, t->code_len, lo, ntiles, tc);
+          k_part_scan<<<1, 1024, 0, s>>>(tc, ntiles, tt);
+          k_hwt_alive_scatter<IT, OT><<<ntiles, HA_THREADS, 0, s>>>((const IT *)d_seq, n, t->code_len, pad, lo,
+                                                                    h - hi, tc, (OT *)Xg);
+        };
+        auto run_in = [&](auto in_tag) {
+          if (kw == 1) run(in_tag, uint8_t{});
+          else if (kw == 2) run(in_tag, uint16_t{});
+          else run(in_tag, uint32_t{});
+        };
+        if (eb == 1) run_in(uint8_t{});
+        else if (eb == 2) run_in(uint16_t{});
+        else run_in(uint32_t{});
+        chk(cudaGetLastError());
+      }
+      wt_tree *pt = nullptr;
+      const int rc = build_impl(Xg, nullptr, false, ng, kw, 1ull << hi, stream_v, &pt, false);
+      if (rc != WT_OK) return fail(rc);
+      StageSegs sg_{lo, hi, nullptr, nullptr, {}, {}};
+      uint32_t *seg_src = A.alloc<uint32_t>(pt->total_nodes, false);
+      sg_.dst = A.alloc<uint32_t>(pt->total_nodes, false);
+      sg_.key = A.alloc<uint32_t>(pt->total_nodes, false);
+      uint32_t *alive = A.alloc<uint32_t>(h, false);
+      if (A.fail) { wt_free(pt); return fail(WT_ENOMEM); }
+      k_hwt_segments<<<hi - lo, 1024, 0, s>>>(pt->level_node_ptr, pt->node_key, pt->node_start, ng, canon, info,
+                                              seg_src, sg_.dst, sg_.key, alive, err, lo);
+      chk(cudaGetLastError());
+      chk(cudaMemcpyAsync(stage, pt->level_node_ptr, (hi + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      chk(cudaMemcpyAsync(stage + 64, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      chk(cudaMemcpyAsync(stage + 128, alive + lo, (hi - lo) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      chk(cudaStreamSynchronize(s));
+      if (ce != cudaSuccess || (uint32_t)stage[64]) { wt_free(pt); return fail(WT_ECUDA); }
+      const uint32_t *h_alive = reinterpret_cast<const uint32_t *>(stage + 128);
+      lv.lbase = lo;
+      uint64_t maxw = 0;
+      for (uint32_t l = lo; l < hi; l++) {
+        lv.segbase[l] = sg_.base[l] = stage[l];
+        lv.nseg[l] = sg_.cnt[l] = h_alive[l - lo];
+        h_np[l + 1] = h_alive[l - lo];  // counts for now, prefix-summed below
+        maxseg = std::max(maxseg, h_alive[l - lo]);
+        maxw = std::max(maxw, h_wp[l + 1] - h_wp[l]);
+      }
+      if (maxw) {
+        const uint64_t per = (uint64_t)HB_WORDS * HB_WPT;
+        k_hwt_bits<<<dim3((unsigned)((maxw + per - 1) / per), hi - lo), HB_WORDS, 0, s>>>(
+            lv, pt->bits, pt->words_per_level, seg_src, sg_.dst, t->bits);
+        chk(cudaGetLastError());
+      }
+      done.push_back(sg_);
+      const int frc = wt_free(pt);  // stream-ordered after the kernels above; synchronises
+      if (frc != WT_OK) return fail(WT_ECUDA);
+    }
+    for (uint32_t l = 0; l < h; l++) h_np[l + 1] += h_np[l];
     t->total_nodes = h_np[h];
     t->node_key = A.alloc<uint32_t>(t->total_nodes, true);
     t->node_start = A.alloc<uint32_t>(t->total_nodes, true);
-    if (A.fail) { wt_free(pt); return fail(WT_ENOMEM); }
+    if (A.fail) return fail(WT_ENOMEM);
     chk(cudaMemcpyAsync(t->level_node_ptr, h_np, (h + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-    k_hwt_nodes<<<dim3(std::min<uint32_t>((maxseg + 255) / 256, 1024), h), 256, 0, s>>>(
-        lv, t->level_node_ptr, seg_key, seg_dst, t->node_key, t->node_start);
-    chk(cudaGetLastError());
-    uint64_t maxw = 0;
-    for (uint32_t l = 0; l < h; l++) maxw = std::max(maxw, h_wp[l + 1] - h_wp[l]);
-    if (maxw) {
-      const uint64_t per = (uint64_t)HB_WORDS * HB_WPT;
-      k_hwt_bits<<<dim3((unsigned)((maxw + per - 1) / per), h), HB_WORDS, 0, s>>>(lv, pt->bits, pt->words_per_level,
-                                                                                  seg_src, seg_dst, t->bits);
+    for (const auto &d : done) {
+      lv.lbase = d.lo;
+      for (uint32_t l = d.lo; l < d.hi; l++) { lv.segbase[l] = d.base[l]; lv.nseg[l] = d.cnt[l]; }
+      k_hwt_nodes<<<dim3(std::min<uint32_t>((maxseg + 255) / 256, 1024), d.hi - d.lo), 256, 0, s>>>(
+          lv, t->level_node_ptr, d.key, d.dst, t->node_key, t->node_start);
       chk(cudaGetLastError());
     }
     // ---- rank directory of all levels ----
@@ -1349,15 +1422,13 @@ int hwt_build_impl(const void *d_seq, uint64_t n, uint32_t eb, uint64_t sigma, v
     for (uint32_t l = 0; l <= h; l++) { rk.wptr[l] = h_wp[l]; rk.bptr[l] = h_bp[l]; rk.sptr[l] = h_sp[l]; }
     for (uint32_t l = 0; l < h; l++) { rk.nl[l] = h_len[l]; rk.soff[l + 1] = rk.soff[l] + (h_len[l] + 65535) / 65536; }
     uint64_t *suptot = A.alloc<uint64_t>(rk.soff[h], false);
-    if (A.fail) { wt_free(pt); return fail(WT_ENOMEM); }
+    if (A.fail) return fail(WT_ENOMEM);
     if (rk.soff[h]) {
       k_hwt_rank_local<<<(unsigned)((rk.soff[h] * 32 + 255) / 256), 256, 0, s>>>(rk, t->bits, t->rank_block, suptot);
       chk(cudaGetLastError());
     }
     k_hwt_rank_super<<<h, 1024, 0, s>>>(rk, suptot, t->rank_super);
     chk(cudaGetLastError());
-    const int frc = wt_free(pt);  // stream-ordered after the kernels above; synchronises
-    if (frc != WT_OK) return fail(WT_ECUDA);
   } else {
     chk(cudaMemcpyAsync(t->level_node_ptr, h_np, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   }

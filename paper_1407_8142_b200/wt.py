@@ -442,7 +442,7 @@ class _HwtTree(ctypes.Structure):
         ("level_node_ptr", ctypes.c_void_p), ("node_key", ctypes.c_void_p), ("node_start", ctypes.c_void_p),
         ("total_nodes", ctypes.c_uint64),
         ("code", ctypes.c_void_p), ("code_len", ctypes.c_void_p),
-        ("only_symbol", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+        ("only_symbol", ctypes.c_uint32), ("stages", ctypes.c_uint32),
         ("total_bits", ctypes.c_uint64),
         ("internal", ctypes.c_void_p),
     ]
@@ -480,6 +480,7 @@ class HuffmanWaveletTree:
         self.n, self.sigma, self.levels = int(t.n), int(t.sigma), int(t.levels)
         self.total_nodes, self.total_bits = int(t.total_nodes), int(t.total_bits)
         self.only_symbol = int(t.only_symbol)
+        self.stages = int(t.stages)
         h = self.levels
         u8 = lambda p, c: _view(p, c, "<u8", torch.uint64, device)  # noqa: E731
         self.level_len = u8(t.level_len, h)

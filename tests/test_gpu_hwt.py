@@ -72,7 +72,7 @@ def test_hwt_shapes(shape):
         S = gen.zipf_permuted(300000, 11)
     elif shape == "geometric":
         S = np.minimum(rng.geometric(0.2, 200000) - 1, 255).astype(np.uint8)
-    elif shape == "fibonacci":  # path-shaped tree, depth 24
+    elif shape == "fibonacci":  # path-shaped tree, depth 24 (staged build)
         fib = [1, 1]
         while len(fib) < 25:
             fib.append(fib[-1] + fib[-2])
@@ -127,4 +127,18 @@ def test_hwt_full_config(cfg_idx):
     S = gen.config_input(cfg)
     t = _compare(S, cfg.sigma)
     _queries(t, S, cfg.sigma, k=2000, seed=cfg_idx)
+    t.free()
+
+
+@pytest.mark.parametrize("s,n,sigma,dtype", [(2.0, 300000, 65536, np.uint16), (1.3, 200000, 4096, np.uint16),
+                                             (3.0, 100000, 65536, np.uint32), (1.6, 150000, 1000, np.uint16)])
+def test_hwt_staged(s, n, sigma, dtype):
+    # skewed codes longer than 8 bits: the staged build (8-level stages over the
+    # elements still alive), checked array by array and by queries
+    S = np.minimum(np.random.default_rng(int(s * 10)).zipf(s, n) - 1, sigma - 1).astype(dtype)
+    t = _compare(S, sigma)
+    assert t.levels > 8
+    if s >= 2.0:
+        assert t.stages > 1  # most elements leave within the first 8 levels
+    _queries(t, S, sigma, k=1500, seed=1)
     t.free()
