@@ -690,7 +690,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
 // ===================== wavelet matrix =====================
 struct WmLaunch {
   void (*kern)(GroupParams) = nullptr;
-  int grid = 0;
+  int grid = 0, block = 32;
   uint32_t tile = 0;
 };
 
@@ -699,10 +699,17 @@ WmLaunch wm_launch() {
   static WmLaunch wl;
   static std::once_flag f;
   std::call_once(f, [] {
+#ifdef WT_WM_WARP  // the one-warp pass (kept for comparison)
     wl.kern = k_wm_group<InT, RecT, OutT, HAS_OUT>;
     wl.tile = WmTile<RecT>::TW;
+    wl.block = 32;
+#else
+    wl.kern = k_wm_group4<InT, RecT, OutT, HAS_OUT>;
+    wl.tile = WmSmem4<RecT, HAS_OUT>::TT;
+    wl.block = WPB * 32;
+#endif
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wl.kern, 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wl.kern, wl.block, 0);
     wl.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
   });
   return wl;
@@ -859,7 +866,7 @@ int wm_build_impl(const void *d_seq, uint64_t n, uint32_t eb, uint64_t sigma, vo
     gp.bits = m->bits;
     gp.wpl = WPL;
     gp.err = err;
-    gr.wl.kern<<<gr.wl.grid, 32, 0, s>>>(gp);
+    gr.wl.kern<<<gr.wl.grid, gr.wl.block, 0, s>>>(gp);
     chk(cudaGetLastError());
     if (NSD) {  // rank block counts of this group's levels on the side stream
       cudaEvent_t ev;
