@@ -7,8 +7,9 @@
 // one warp, with no global counts: the row's own digit histogram gives every
 // node start below it.  A warp takes a BATCH of consecutive rows (those whose
 // start lies in one TW-sized window of positions); the batch covers a
-// contiguous range [A, B) at each of the tau levels, so its bits are staged in
-// shared memory and written with only the two edge words shared (A5).
+// contiguous range [A, B) at each of the tau levels, so each level's bits are
+// assembled word by word as the rows arrive (lane k owns level k's word) and
+// written with only the two edge words shared (A5).
 //
 // Per row:
 //  * <= 32 symbols: register path, one symbol per lane, no data movement: the
@@ -66,9 +67,9 @@ constexpr uint32_t DEFER_W = 1 + TAU_MAX;  // u32 per deferred row
 template <typename RecT, int MODE>
 struct LocalSmem {
   static constexpr uint32_t BUFN = MODE == LM_COUNT ? 1 : (MODE == LM_BUILD ? LT : TW);
-  static constexpr uint32_t SBW = MODE == LM_COUNT ? 1 : (MODE == LM_BUILD ? 2 * NCH + 2 : NCH + 2);
   alignas(16) RecT buf[2][BUFN];
-  alignas(16) uint32_t SB[TAU_MAX][SBW];  // batch staging bitmaps
+  unsigned long long acc[TAU_MAX];  // per level: the output word being assembled ...
+  uint32_t accw[TAU_MAX];           // ... and its index (rows arrive in position order)
   alignas(16) uint32_t LB[MODE == LM_COUNT ? 1 : BUFN / 32];
   uint32_t hist2[NDIG / 2];
   uint16_t Hl[NDIG + 2];
@@ -77,11 +78,39 @@ struct LocalSmem {
 
 constexpr int LOCAL_WARPS = 2;
 
-// OR `nbits` (<= 32) bits of v into the staging bitmap at bit offset `off`.
-__device__ __forceinline__ void stage_bits(uint32_t *SB, uint32_t off, uint32_t v) {
-  const uint32_t w = off >> 5, sh = off & 31;
-  SB[w] |= v << sh;
-  if (sh) SB[w + 1] |= v >> (32 - sh);
+// Level-bit output of a batch [A, Bend): bits arrive in position order and are
+// assembled word by word per level; a word that lies wholly inside the batch
+// is stored, a word shared with a neighbouring batch (or with a row the build
+// pass deferred) is OR-ed in (A5: only edge words are shared).
+__device__ __forceinline__ void acc_flush(unsigned long long v, uint32_t gw, uint64_t *Bw, uint32_t A, uint32_t Bend,
+                                          uint64_t n) {
+  if (gw == 0xffffffffu) return;
+  const uint64_t lo = (uint64_t)gw * 64, hi = lo + 64, hic = hi < n ? hi : n;
+  if ((uint64_t)A <= lo && (uint64_t)Bend >= hic) Bw[gw] = v;
+  else if (v) atomicOr(reinterpret_cast<unsigned long long *>(&Bw[gw]), v);
+}
+
+// append nb (<= 32) bits v (zero above nb) at global bit g of level k
+template <typename WS>
+__device__ __forceinline__ void acc_put(WS &ws, uint32_t k, uint32_t g, uint32_t v, uint32_t nb, uint64_t *Bw,
+                                        uint32_t A, uint32_t Bend, uint64_t n) {
+  if (!nb) return;
+  const uint32_t gw = g >> 6, sh = g & 63;
+  unsigned long long a = ws.acc[k];
+  uint32_t w = ws.accw[k];
+  if (gw != w) {
+    acc_flush(a, w, Bw, A, Bend, n);
+    a = 0;
+    w = gw;
+  }
+  a |= (unsigned long long)v << sh;
+  if (sh + nb > 64) {
+    acc_flush(a, w, Bw, A, Bend, n);
+    a = (unsigned long long)v >> (64 - sh);
+    w = gw + 1;
+  }
+  ws.acc[k] = a;
+  ws.accw[k] = w;
 }
 
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT, int MODE>
@@ -117,10 +146,12 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
       if (lane == 0) atomicOr(p.err, 2u);
       continue;
     }
-    const uint32_t nsw = ((Bend - A) + 31) / 32 + 1;  // staging words used
-    if (!COUNT) {
-      for (uint32_t k = 0; k < tau; k++)
-        for (uint32_t w = lane; w < nsw; w += 32) ws.SB[k][w] = 0;
+    uint64_t *Bl = p.bits + (uint64_t)(p.l0 + (lane < (int)tau ? lane : 0)) * p.wpl;  // lane k: level l0+k
+    if constexpr (!COUNT) {
+      if (lane < (int)tau) {
+        ws.acc[lane] = 0;
+        ws.accw[lane] = 0xffffffffu;
+      }
     }
     // running node offsets (lane kk holds level l0+1+kk), from the batch scan
     uint32_t nodeoff = 0;
@@ -143,20 +174,20 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
         kA_n = rs_n + lane < p.n ? (uint32_t)keys[rs_n + lane] : 0u;
         kB_n = rs_n + 32 + lane < p.n ? (uint32_t)keys[rs_n + 32 + lane] : 0u;
       }
-      const uint32_t soff = rs - A;  // the row's bit offset inside the batch staging
       if (len <= 32) {
         // ---------------- register path ----------------
         const bool valid = (uint32_t)lane < len;
         const uint32_t key = valid ? kA0 : 0u;
         const uint32_t dig = (key >> pbits) & (ndig - 1u);
         uint32_t eq = __ballot_sync(FULL, valid), ltm = 0;  // same prefix / smaller prefix (this row)
+        uint32_t myw = 0;                                    // lane k: the row's word of level l0+k
         for (uint32_t k = 0; k < tau; k++) {
           const uint32_t bit = (dig >> (tau - 1u - k)) & 1u;
           const uint32_t m = __ballot_sync(FULL, valid && bit);
           if (!COUNT) {
             const uint32_t pos = __popc(ltm) + __popc(eq & lt);  // position at level l0+k
             const uint32_t word = __reduce_or_sync(FULL, valid && bit ? (1u << pos) : 0u);
-            if (lane == 0) stage_bits(ws.SB[k], soff, word);
+            if (lane == (int)k) myw = word;
           }
           // refine to the (k+1)-bit prefix: same group and same bit; smaller if bit 0 vs my 1
           if (bit) {
@@ -178,6 +209,8 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
           }
         }
         if (HAS_OUT && !COUNT && valid) ko[rs + __popc(ltm) + __popc(eq & lt)] = (OutT)(key & pmask);
+        if (!COUNT && lane < (int)tau) acc_put(ws, lane, rs, myw, len, Bl, A, Bend, p.n);
+        __syncwarp();
         continue;
       }
       if (len <= 64) {
@@ -191,6 +224,7 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
         const uint64_t valid64 = ((uint64_t)__ballot_sync(FULL, vB) << 32) | 0xffffffffull;
         const uint64_t befA = (uint64_t)lt, befB = 0xffffffffull | ((uint64_t)lt << 32);
         uint64_t eqA = valid64, eqB = valid64, ltA = 0, ltB = 0;
+        uint32_t mylo = 0, myhi = 0;  // lane k: the row's words of level l0+k
         for (uint32_t k = 0; k < tau; k++) {
           const uint32_t bA = (dA >> (tau - 1u - k)) & 1u, bB = (dB >> (tau - 1u - k)) & 1u;
           const uint64_t M = ((uint64_t)__ballot_sync(FULL, vB && bB) << 32) | __ballot_sync(FULL, vA && bA);
@@ -202,10 +236,7 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
             if (vB && bB) { if (pB < 32) lo |= 1u << pB; else hi |= 1u << (pB - 32); }
             lo = __reduce_or_sync(FULL, lo);
             hi = __reduce_or_sync(FULL, hi);
-            if (lane == 0) {
-              stage_bits(ws.SB[k], soff, lo);
-              stage_bits(ws.SB[k], soff + 32, hi);
-            }
+            if (lane == (int)k) { mylo = lo; myhi = hi; }
           }
           if (bA) { ltA |= eqA & ~M; eqA &= M; } else { eqA &= ~M; }
           if (bB) { ltB |= eqB & ~M; eqB &= M; } else { eqB &= ~M; }
@@ -231,6 +262,11 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
           ko[rs + __popcll(ltA) + __popcll(eqA & befA)] = (OutT)(kA & pmask);
           if (vB) ko[rs + __popcll(ltB) + __popcll(eqB & befB)] = (OutT)(kB & pmask);
         }
+        if (!COUNT && lane < (int)tau) {
+          acc_put(ws, lane, rs, mylo, 32, Bl, A, Bend, p.n);
+          acc_put(ws, lane, rs + 32, myhi, len - 32, Bl, A, Bend, p.n);
+        }
+        __syncwarp();
         continue;
       }
       // ---------------- tile path (64 < len <= TW) ----------------
@@ -334,12 +370,13 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
           }
         }
         __syncwarp();
-        // the row's level bits are LB[0..len) in order: copy into the batch staging
+        // the row's level bits are LB[0..len) in order: append them to level k's output
         if (lane == 0) {
+          uint64_t *Bk = p.bits + (uint64_t)(p.l0 + k) * p.wpl;
           for (uint32_t ci = 0; ci < nch; ci++) {
             const uint32_t nb = min(32u, len - ci * 32);
             const uint32_t v = nb == 32 ? ws.LB[ci] : (ws.LB[ci] & ((1u << nb) - 1u));
-            stage_bits(ws.SB[k], soff + ci * 32, v);
+            acc_put(ws, k, rs + ci * 32, v, nb, Bk, A, Bend, p.n);
           }
         }
         __syncwarp();
@@ -351,23 +388,8 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
       continue;
     }
     __syncwarp();
-    // ---- the batch's bits [A, Bend) of each level -> global; only edge words shared ----
-    for (uint32_t k = 0; k < tau; k++) {
-      uint64_t *Bw = p.bits + (uint64_t)(p.l0 + k) * p.wpl;
-      const uint64_t g0 = A >> 6, g1 = ((uint64_t)Bend - 1) >> 6;
-      for (uint64_t gw = g0 + lane; gw <= g1; gw += 32) {
-        // 64 bits of staging starting at local bit (gw*64 - A)
-        const int base = (int)((int64_t)gw * 64 - (int64_t)A);
-        uint64_t v = extract64(ws.SB[k], base, (int)nsw);
-        const uint64_t lo = gw * 64, hi = lo + 64;
-        const uint64_t s0 = (uint64_t)A > lo ? (uint64_t)A - lo : 0;
-        const uint64_t e0 = (uint64_t)Bend < hi ? (uint64_t)Bend - lo : 64;
-        v &= (e0 - s0 == 64) ? ~0ull : (((1ull << (e0 - s0)) - 1ull) << s0);
-        const uint64_t hi_clip = hi < p.n ? hi : p.n;
-        if ((uint64_t)A <= lo && (uint64_t)Bend >= hi_clip) Bw[gw] = v;
-        else if (v) atomicOr(reinterpret_cast<unsigned long long *>(&Bw[gw]), (unsigned long long)v);
-      }
-    }
+    // ---- the last assembled word of each level ----
+    if (lane < (int)tau) acc_flush(ws.acc[lane], ws.accw[lane], Bl, A, Bend, p.n);
     __syncwarp();
   }
 }
