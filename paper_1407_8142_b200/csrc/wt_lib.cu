@@ -407,12 +407,10 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   uint32_t *ncount = A.alloc<uint32_t>(L + 1, false);
   uint64_t *suptot = A.alloc<uint64_t>(L * NSD, false);
 
-  static uint64_t *h_stage = nullptr;  // pinned staging for the single D2H
-  static std::mutex stage_mu;
-  {
-    std::lock_guard<std::mutex> g(stage_mu);
-    if (!h_stage && cudaMallocHost(&h_stage, 64 * sizeof(uint64_t)) != cudaSuccess) A.fail = true;
-  }
+  // pinned staging for the single D2H; one per host thread, so that builds
+  // issued concurrently from several threads do not share it
+  static thread_local uint64_t *h_stage = nullptr;
+  if (!h_stage && cudaMallocHost(&h_stage, 64 * sizeof(uint64_t)) != cudaSuccess) A.fail = true;
   if (A.fail) {
     A.free_scratch();
     A.free_outputs();
@@ -894,11 +892,14 @@ int wm_build_impl(const void *d_seq, uint64_t n, uint32_t eb, uint64_t sigma, vo
     k_wm_zeros<<<(L + 31) / 32, 32, 0, s>>>(m->rank_super, SPL, L, n, m->zeros, err);
     chk(cudaGetLastError());
   }
-  static uint32_t *h_err = nullptr;
-  static std::mutex mu;
-  {
-    std::lock_guard<std::mutex> gl(mu);
-    if (!h_err) cudaMallocHost(&h_err, sizeof(uint32_t) * 4);
+  static thread_local uint32_t *h_err = nullptr;  // pinned, one per host thread
+  if (!h_err && cudaMallocHost(&h_err, sizeof(uint32_t) * 4) != cudaSuccess) h_err = nullptr;
+  if (!h_err) {
+    A.free_scratch();
+    A.free_outputs();
+    cudaStreamSynchronize(s);
+    delete m;
+    return WT_ENOMEM;
   }
   chk(cudaMemcpyAsync(h_err, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   A.free_scratch();
@@ -1139,12 +1140,9 @@ struct HwtInternal {
   HuffCanon *canon = nullptr;
 };
 
-uint64_t *hwt_stage() {  // pinned staging for the host reads of hwt_build
-  static uint64_t *st = nullptr;
-  static std::once_flag f;
-  std::call_once(f, [] {
-    if (cudaMallocHost(&st, 256 * sizeof(uint64_t)) != cudaSuccess) st = nullptr;
-  });
+uint64_t *hwt_stage() {  // pinned staging for the host reads of hwt_build (one per host thread)
+  static thread_local uint64_t *st = nullptr;
+  if (!st && cudaMallocHost(&st, 256 * sizeof(uint64_t)) != cudaSuccess) st = nullptr;
   return st;
 }
 
