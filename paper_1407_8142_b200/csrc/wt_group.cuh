@@ -423,7 +423,8 @@ __global__ void __launch_bounds__(WPB * 32, WT_GMINB) k_group(GroupParams p) {
       if (warp == 0) digit_exscan(s.BX, ndig, lane);
     }
 
-    for (uint32_t start = cbeg; start < cend; start += TT) {
+    for (uint64_t start64 = cbeg; start64 < cend; start64 += TT) {  // 64-bit: cend may be near 2^32
+      const uint32_t start = (uint32_t)start64;
       PH(0);
       const uint32_t rem = cend - start;
       const uint32_t len = rem < (uint32_t)TT ? rem : (uint32_t)TT;

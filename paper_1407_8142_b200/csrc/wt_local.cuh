@@ -162,8 +162,8 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
 
     // the next row's start, key and first 64 symbols are loaded one row ahead
     uint32_t rs_n = A, re_n = r0 + 1 < nrows ? p.row_start[r0 + 1] : (uint32_t)p.n, P_n = p.row_key[r0];
-    uint32_t kA_n = rs_n + lane < p.n ? (uint32_t)keys[rs_n + lane] : 0u;
-    uint32_t kB_n = rs_n + 32 + lane < p.n ? (uint32_t)keys[rs_n + 32 + lane] : 0u;
+    uint32_t kA_n = (uint64_t)rs_n + lane < p.n ? (uint32_t)keys[(uint64_t)rs_n + lane] : 0u;
+    uint32_t kB_n = (uint64_t)rs_n + 32 + lane < p.n ? (uint32_t)keys[(uint64_t)rs_n + 32 + lane] : 0u;
     for (uint32_t r = r0; r < r1; r++) {
       const uint32_t rs = rs_n, re = re_n, P = P_n, kA0 = kA_n, kB0 = kB_n;
       const uint32_t len = re - rs;
@@ -171,8 +171,8 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
         rs_n = re;
         re_n = r + 2 < nrows ? p.row_start[r + 2] : (uint32_t)p.n;
         P_n = p.row_key[r + 1];
-        kA_n = rs_n + lane < p.n ? (uint32_t)keys[rs_n + lane] : 0u;
-        kB_n = rs_n + 32 + lane < p.n ? (uint32_t)keys[rs_n + 32 + lane] : 0u;
+        kA_n = (uint64_t)rs_n + lane < p.n ? (uint32_t)keys[(uint64_t)rs_n + lane] : 0u;
+        kB_n = (uint64_t)rs_n + 32 + lane < p.n ? (uint32_t)keys[(uint64_t)rs_n + 32 + lane] : 0u;
       }
       if (len <= 32) {
         // ---------------- register path ----------------

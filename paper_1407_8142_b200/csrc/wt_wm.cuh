@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(32) k_wm_group(GroupParams p) {
     digit_exscan(s.BX, ndig, lane);
     __syncwarp();
 
-    for (uint32_t start = cbeg; start < cend; start += TWT) {
+    for (uint64_t start64 = cbeg; start64 < cend; start64 += TWT) {  // 64-bit: cend may be near 2^32
+      const uint32_t start = (uint32_t)start64;
       const uint32_t rem = cend - start;
       const uint32_t len = rem < (uint32_t)TWT ? rem : (uint32_t)TWT;
       for (uint32_t d = lane; d < NDIG; d += 32) s.H[d] = 0u;
@@ -486,7 +487,8 @@ __global__ void __launch_bounds__(WPB * 32, 4) k_wm_group4(GroupParams p) {
     __syncthreads();
     if (warp == 0) digit_exscan(s.BX, ndig, lane);
 
-    for (uint32_t start = cbeg; start < cend; start += TT) {
+    for (uint64_t start64 = cbeg; start64 < cend; start64 += TT) {  // 64-bit: cend may be near 2^32
+      const uint32_t start = (uint32_t)start64;
       const uint32_t rem = cend - start;
       const uint32_t len = rem < (uint32_t)TT ? rem : (uint32_t)TT;
       for (uint32_t d = tid; d < NDIG; d += WPB * 32) s.H[d] = 0u;
