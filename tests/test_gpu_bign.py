@@ -107,3 +107,32 @@ def test_n_near_2_32_sigma_2_16(structure):
     want = (pos >> 16) * cnt[sy] + inpart
     assert np.array_equal(got.astype(np.int64), want)
     t.free()
+
+
+def test_hwt_n_near_2_32():
+    import paper_1407_8142_b200 as wt
+    free, total = torch.cuda.mem_get_info()
+    if total < 64 << 30:
+        pytest.skip("needs a large-memory GPU")
+    # skewed 8-symbol pattern: codes of lengths 1..7
+    P = np.minimum(np.random.default_rng(3).geometric(0.5, 1 << 16) - 1, 7).astype(np.uint8)
+    n = (1 << 32) - 999
+    reps = (n + (1 << 16) - 1) >> 16
+    S = torch.from_numpy(P).cuda().repeat(reps)[:n].contiguous()
+    t = wt.hwt_build(S, 8)
+    cnt = np.bincount(P, minlength=8).astype(np.int64)
+    tot = cnt * (n >> 16) + np.bincount(P[:n & 0xFFFF], minlength=8)
+    ln = t.code_len.cpu().numpy().astype(np.int64)
+    assert t.total_bits == int((tot * ln).sum())
+    assert t.level_len.cpu().numpy().astype(np.int64).tolist() == [int(tot[ln > l].sum()) for l in range(t.levels)]
+    rng = np.random.default_rng(12)
+    pos = np.concatenate([rng.integers(0, n, 20000), np.arange(n - 3000, n)])
+    acc = t.access(torch.from_numpy(pos.astype(np.int64)).cuda()).cpu().numpy()
+    assert np.array_equal(acc, P[pos & 0xFFFF].astype(np.uint32))
+    sy = rng.integers(0, 8, pos.size).astype(np.int64)
+    got = t.rank(torch.from_numpy(sy.astype(np.int32)).cuda(), torch.from_numpy(pos.astype(np.int64)).cuda()).cpu().numpy()
+    pre = np.zeros((8, (1 << 16) + 1), dtype=np.int64)
+    for c in range(8):
+        pre[c, 1:] = np.cumsum(P == c)
+    assert np.array_equal(got.astype(np.int64), (pos >> 16) * cnt[sy] + pre[sy, (pos & 0xFFFF) + 1])
+    t.free()
