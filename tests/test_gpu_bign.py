@@ -51,6 +51,14 @@ def test_n_near_2_32():
         pre[c, 1:] = np.cumsum(P == c)
     want = (pos >> 16) * cnt[sym] + pre[sym, (pos & 0xFFFF) + 1]
     assert np.array_equal(got.astype(np.int64), want)
+    # select_c(k) (1-based k): full periods of the pattern plus the r-th occurrence in it
+    occ = [np.nonzero(P == c)[0] for c in range(4)]
+    ks = np.concatenate([rng.integers(1, tot[s] + 1, 500) for s in range(4)] + [tot[:4]])
+    cs = np.concatenate([np.full(500, s) for s in range(4)] + [np.arange(4)]).astype(np.int64)
+    sel = t.select(torch.from_numpy(cs.astype(np.int32)).cuda(), torch.from_numpy(ks.astype(np.int64)).cuda())
+    q, r = (ks - 1) // cnt[cs], (ks - 1) % cnt[cs]
+    want_sel = q * (1 << 16) + np.array([occ[c][i] for c, i in zip(cs, r)])
+    assert np.array_equal(sel.cpu().numpy().astype(np.int64), want_sel)
     t.free()
 
 
