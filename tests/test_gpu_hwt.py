@@ -142,3 +142,18 @@ def test_hwt_staged(s, n, sigma, dtype):
         assert t.stages > 1  # most elements leave within the first 8 levels
     _queries(t, S, sigma, k=1500, seed=1)
     t.free()
+
+
+@pytest.mark.parametrize("dtype,sigma", [(np.uint8, 200), (np.uint16, 3000), (np.uint32, 70000 - 4465)])
+def test_hwt_unaligned_device_pointer(dtype, sigma):
+    S = np.minimum(np.random.default_rng(9).zipf(1.5, 50001) - 1, sigma - 1).astype(dtype)
+    base = torch.from_numpy(S).cuda()
+    for off in (1, 2):
+        v = base[off:]
+        assert v.data_ptr() % 16 != 0
+        import paper_1407_8142_b200 as wt
+        t = wt.hwt_build(v, sigma)
+        got, want = t.numpy(), oracle.hwt_build(S[off:].copy(), sigma)
+        for k in KEYS:
+            assert np.array_equal(got[k], want[k]), (off, k)
+        t.free()

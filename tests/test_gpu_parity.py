@@ -238,3 +238,14 @@ def test_local_rows_exact_sizes(sizes):
     S = np.concatenate(parts)
     rng.shuffle(S)
     _compare(S, 1 << 16)
+
+
+@pytest.mark.parametrize("dtype,sigma", [(np.uint8, 256), (np.uint16, 40000), (np.uint32, 1 << 24)])
+@pytest.mark.parametrize("off", [1, 3, 7])
+def test_unaligned_narrow_types(dtype, sigma, off):
+    wt = _wt()
+    S = gen.uniform_below(90001, sigma, seed=off, dtype=dtype)
+    v = torch.from_numpy(S).cuda()[off:]
+    tree = wt.build(v, sigma)
+    _compare(S[off:].copy(), sigma, tree)
+    tree.free()

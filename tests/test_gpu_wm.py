@@ -75,3 +75,19 @@ def test_wm_full_config(cfg_idx):
     cfg = gen.CONFIGS[cfg_idx]
     S = gen.config_input(cfg)
     _compare(S, cfg.sigma).free()
+
+
+@pytest.mark.parametrize("dtype,sigma", [(np.uint8, 200), (np.uint16, 3000), (np.uint32, 1 << 20)])
+def test_wm_unaligned_device_pointer(dtype, sigma):
+    import paper_1407_8142_b200 as wt
+    S = gen.uniform_below(70001, sigma, seed=5, dtype=dtype)
+    base = torch.from_numpy(S).cuda()
+    for off in (1, 3):
+        v = base[off:]
+        assert v.data_ptr() % 16 != 0
+        m = wt.wm_build(v, sigma)
+        want = oracle.wm_build(S[off:], sigma)
+        got = m.numpy()
+        for k in KEYS:
+            assert np.array_equal(got[k], want[k]), (off, k)
+        m.free()
