@@ -6,7 +6,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = [os.path.join(HERE, "csrc", "wt_lib.cu")]
+SRC = [os.path.join(HERE, "csrc", f) for f in ("wt_lib.cu", "wm_lib.cu", "hwt_lib.cu", "dist_lib.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + \
     [os.path.join(ROOT, "include", "wt.h")]
 LIB = os.path.join(HERE, "libwt_b200.so")

@@ -18,7 +18,7 @@ constexpr uint32_t FLAG_INC = 2u << 30;  // lookback: inclusive prefix published
 constexpr uint32_t VAL_MASK = (1u << 30) - 1;
 
 #ifdef WT_DEBUG
-__device__ uint32_t g_wt_dbg[4];
+static __device__ uint32_t g_wt_dbg[4];
 #define WT_CHECK(cond, code)                                                        \
   do {                                                                              \
     if (!(cond)) {                                                                  \

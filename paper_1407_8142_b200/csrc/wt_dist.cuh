@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(PART_THREADS) k_part_hist(const T *__restrict_
 }
 
 // One CTA per digit: exclusive scan of its tile counts in place; tot[d] = total.
-__global__ void __launch_bounds__(1024) k_part_scan(uint32_t *__restrict__ thT, uint32_t ntiles,
+static __global__ void __launch_bounds__(1024) k_part_scan(uint32_t *__restrict__ thT, uint32_t ntiles,
                                                    uint64_t *__restrict__ tot) {
   __shared__ uint32_t shm[33];
   uint32_t *row = thT + (uint64_t)blockIdx.x * ntiles;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(PART_THREADS) k_part_scatter(const T *__restri
 // ---------------------------------------------------------------------------
 constexpr uint32_t GB_WORDS = 256, GB_WPT = 8, GB_SEGS = 1024;
 
-__global__ void __launch_bounds__(GB_WORDS) k_gather_bits(const uint64_t *__restrict__ src,
+static __global__ void __launch_bounds__(GB_WORDS) k_gather_bits(const uint64_t *__restrict__ src,
                                                           const uint64_t *__restrict__ segs, uint64_t nseg,
                                                           uint64_t *__restrict__ dst, uint64_t dst_words) {
   __shared__ unsigned long long s_d[GB_SEGS], s_s[GB_SEGS], s_l[GB_SEGS];

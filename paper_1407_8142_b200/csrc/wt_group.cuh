@@ -60,7 +60,7 @@ struct GroupParams {
 };
 
 #ifdef WT_PHASES
-__device__ unsigned long long g_ph[16];
+static __device__ unsigned long long g_ph[16];
 #define PH_DECL                            \
   unsigned long long ph_t = clock64();     \
   unsigned long long ph_acc[12];           \

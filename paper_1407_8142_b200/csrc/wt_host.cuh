@@ -1,0 +1,176 @@
+// wt_host.cuh -- host-side helpers shared by the translation units of
+// libwt_b200.so (wt_lib.cu: the tree; wm_lib.cu: the matrix; hwt_lib.cu: the
+// Huffman-shaped tree; dist_lib.cu: the sharded-build helpers): per-build
+// launch recorder, stream-ordered allocations, device queries.
+#pragma once
+#include "wt.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace wtb {
+struct TreeView;
+}
+
+namespace wthost {
+
+struct Prof {
+  bool enabled = false;
+  wt_profile last{};
+  std::mutex mu;
+};
+inline Prof g_prof;
+
+struct Launch {
+  std::string name;
+  uint64_t algo_bytes;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+// Per-build recorder of kernel launches (optionally timed with events).
+struct Recorder {
+  cudaStream_t s;
+  bool timed;
+  std::vector<Launch> launches;
+  explicit Recorder(cudaStream_t st, bool t) : s(st), timed(t) {}
+  cudaStream_t cur = nullptr;
+  void begin(const char *name, uint64_t bytes, cudaStream_t on = nullptr) {
+    Launch L;
+    L.name = name;
+    L.algo_bytes = bytes;
+    cur = on ? on : s;
+    if (timed) {
+      cudaEventCreate(&L.e0);
+      cudaEventCreate(&L.e1);
+      cudaEventRecord(L.e0, cur);
+    }
+    launches.push_back(L);
+  }
+  void end() {
+    if (timed) cudaEventRecord(launches.back().e1, cur);
+  }
+  void publish() {  // after the stream has been synchronised
+    wt_profile p{};
+    p.total_launches = (uint32_t)launches.size();
+    for (auto &L : launches) {
+      float ms = 0.f;
+      if (timed) {
+        cudaEventElapsedTime(&ms, L.e0, L.e1);
+        cudaEventDestroy(L.e0);
+        cudaEventDestroy(L.e1);
+      }
+      int k = -1;
+      for (uint32_t i = 0; i < p.count; i++)
+        if (L.name == p.e[i].name) k = (int)i;
+      if (k < 0 && p.count < WT_PROF_MAX) {
+        k = (int)p.count++;
+        snprintf(p.e[k].name, sizeof(p.e[k].name), "%s", L.name.c_str());
+      }
+      if (k >= 0) {
+        p.e[k].ms += ms;
+        p.e[k].launches += 1;
+        p.e[k].algo_bytes += L.algo_bytes;
+      }
+    }
+    std::lock_guard<std::mutex> g(g_prof.mu);
+    g_prof.last = p;
+  }
+  void discard() {
+    if (timed)
+      for (auto &L : launches) {
+        cudaEventDestroy(L.e0);
+        cudaEventDestroy(L.e1);
+      }
+  }
+};
+
+struct Internal {
+  cudaStream_t stream;
+  std::vector<void *> outputs;
+};
+
+inline uint32_t levels_of(uint64_t sigma) {
+  uint64_t v = sigma - 1;
+  uint32_t L = 0;
+  while (v) { L++; v >>= 1; }
+  return L;
+}
+
+// A second stream of the same device for the rank directory of finished
+// level groups, so that it overlaps the next group pass (created once).
+inline cudaStream_t side_stream() {
+  static cudaStream_t side = nullptr;
+  static std::once_flag f;
+  std::call_once(f, [] { cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking); });
+  return side;
+}
+
+inline int g_num_sms = 0;
+inline int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+inline void configure_pool_once() {
+  static std::once_flag f;
+  std::call_once(f, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+// Stream-ordered allocations that are released together on error.
+struct Allocs {
+  cudaStream_t s;
+  std::vector<void *> scratch, outputs;
+  bool fail = false;
+  template <typename T>
+  T *alloc(size_t count, bool output) {
+    if (count == 0) count = 1;
+    void *p = nullptr;
+    if (cudaMallocAsync(&p, count * sizeof(T), s) != cudaSuccess) {
+      fail = true;
+      return nullptr;
+    }
+    (output ? outputs : scratch).push_back(p);
+    return static_cast<T *>(p);
+  }
+  void free_scratch() {
+    for (void *p : scratch) cudaFreeAsync(p, s);
+    scratch.clear();
+  }
+  void free_outputs() {
+    for (void *p : outputs) cudaFreeAsync(p, s);
+    outputs.clear();
+  }
+};
+
+// bytes of an unsigned integer holding `bits` bits
+inline uint32_t width_of(uint32_t bits) { return bits <= 8 ? 1u : (bits <= 16 ? 2u : 4u); }
+
+// Defined in wt_lib.cu.  build_impl: the whole wt_build (the Huffman-shaped
+// build runs it on padded codes); select_index_impl: the select directory of
+// one structure (tree or matrix).
+int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n, uint32_t eb, uint64_t sigma,
+               void *stream_v, wt_tree **out, bool force_chain);
+int select_index_impl(const wtb::TreeView &v, uint64_t *sps_out, uint32_t **s0, uint32_t **s1,
+                      std::vector<void *> &owned, cudaStream_t s);
+
+}  // namespace wthost

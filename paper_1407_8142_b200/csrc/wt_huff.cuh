@@ -170,7 +170,7 @@ __device__ __forceinline__ void bitonic_chunk(uint64_t *sk, uint32_t base, uint3
 
 // compact the occurring symbols as keys (freq << 32 | sym) in symbol order,
 // padded with UINT64_MAX to P; info[1] = m (one CTA)
-__global__ void __launch_bounds__(1024) k_huff_compact(const uint32_t *__restrict__ hist, uint32_t sigma,
+static __global__ void __launch_bounds__(1024) k_huff_compact(const uint32_t *__restrict__ hist, uint32_t sigma,
                                                        uint64_t *__restrict__ keys, uint32_t P,
                                                        uint64_t *__restrict__ info) {
   __shared__ uint32_t shm[33];
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(1024) k_huff_compact(const uint32_t *__restric
 // shared memory (one CTA each) for the strides < SORT_CH, one
 // compare-exchange per thread for the larger strides.
 // k == 0: sort each chunk completely (k = 2 .. CH); else strides CH/2 .. 1 of stage k.
-__global__ void __launch_bounds__(1024) k_bitonic_chunk(uint64_t *__restrict__ keys, uint32_t P, uint32_t k) {
+static __global__ void __launch_bounds__(1024) k_bitonic_chunk(uint64_t *__restrict__ keys, uint32_t P, uint32_t k) {
   __shared__ uint64_t sk[SORT_CH];
   const uint32_t CH = P < SORT_CH ? P : SORT_CH;
   const uint32_t c0 = blockIdx.x * CH;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(1024) k_bitonic_chunk(uint64_t *__restrict__ k
   for (uint32_t i = threadIdx.x; i < CH; i += blockDim.x) keys[c0 + i] = sk[i];
 }
 
-__global__ void k_bitonic_step(uint64_t *__restrict__ keys, uint32_t P, uint32_t j, uint32_t k) {
+static __global__ void k_bitonic_step(uint64_t *__restrict__ keys, uint32_t P, uint32_t j, uint32_t k) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // pair index
   if (t >= P / 2) return;
   const uint32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), x = i | j;
@@ -213,7 +213,7 @@ __global__ void k_bitonic_step(uint64_t *__restrict__ keys, uint32_t P, uint32_t
   if ((a > b) == ((i & k) == 0)) { keys[i] = b; keys[x] = a; }
 }
 
-__global__ void __launch_bounds__(1024) k_huff_codes(const uint64_t *__restrict__ keys, uint32_t sigma,
+static __global__ void __launch_bounds__(1024) k_huff_codes(const uint64_t *__restrict__ keys, uint32_t sigma,
                                                      uint32_t *__restrict__ scr, uint8_t *__restrict__ code_len,
                                                      uint32_t *__restrict__ code, uint32_t *__restrict__ pad,
                                                      uint32_t *__restrict__ sym_sorted, HuffCanon *canon,
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(512) k_huff_map(const InT *__restrict__ S, uin
 //   alive[l] = number of surviving nodes; err |= 2 when their total length
 //   differs from n_l.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_hwt_segments(const uint64_t *__restrict__ pptr, const uint32_t *__restrict__ pkey,
+static __global__ void __launch_bounds__(1024) k_hwt_segments(const uint64_t *__restrict__ pptr, const uint32_t *__restrict__ pkey,
                                                        const uint32_t *__restrict__ pstart, uint64_t n,
                                                        const HuffCanon *__restrict__ canon, const uint64_t *__restrict__ info,
                                                        uint32_t *__restrict__ seg_src, uint32_t *__restrict__ seg_dst,
@@ -578,7 +578,7 @@ struct HwtLevels {
 // ---------------------------------------------------------------------------
 constexpr uint32_t HB_WORDS = 256, HB_WPT = 8, HB_SEGS = 2048;
 
-__global__ void __launch_bounds__(HB_WORDS) k_hwt_bits(HwtLevels lv, const uint64_t *__restrict__ pbits, uint64_t pwpl,
+static __global__ void __launch_bounds__(HB_WORDS) k_hwt_bits(HwtLevels lv, const uint64_t *__restrict__ pbits, uint64_t pwpl,
                                                        const uint32_t *__restrict__ seg_src,
                                                        const uint32_t *__restrict__ seg_dst, uint64_t *__restrict__ out) {
   __shared__ uint32_t s_dst[HB_SEGS + 1], s_src[HB_SEGS];
@@ -651,7 +651,7 @@ struct HwtRankLv {
 
 // one warp per (level, data superblock): popcounts of its <= 128 blocks and
 // the in-superblock scan (the per-level layout of k_rank_local)
-__global__ void k_hwt_rank_local(HwtRankLv r, const uint64_t *__restrict__ bits, uint16_t *__restrict__ rank_block,
+static __global__ void k_hwt_rank_local(HwtRankLv r, const uint64_t *__restrict__ bits, uint16_t *__restrict__ rank_block,
                                  uint64_t *__restrict__ suptot) {
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -689,7 +689,7 @@ __global__ void k_hwt_rank_local(HwtRankLv r, const uint64_t *__restrict__ bits,
 }
 
 // one CTA per level: exclusive scan of the superblock totals (+ the total)
-__global__ void __launch_bounds__(1024) k_hwt_rank_super(HwtRankLv r, const uint64_t *__restrict__ suptot,
+static __global__ void __launch_bounds__(1024) k_hwt_rank_super(HwtRankLv r, const uint64_t *__restrict__ suptot,
                                                         uint64_t *__restrict__ rank_super) {
   __shared__ unsigned long long warp_tot[33];
   const uint32_t l = blockIdx.x;
@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(1024) k_hwt_rank_super(HwtRankLv r, const uint
 }
 
 // Node table of the Huffman-shaped tree from the surviving segments.
-__global__ void k_hwt_nodes(HwtLevels lv, const uint64_t *__restrict__ optr, const uint32_t *__restrict__ seg_key,
+static __global__ void k_hwt_nodes(HwtLevels lv, const uint64_t *__restrict__ optr, const uint32_t *__restrict__ seg_key,
                             const uint32_t *__restrict__ seg_dst, uint32_t *__restrict__ node_key,
                             uint32_t *__restrict__ node_start) {
   const uint32_t l = lv.lbase + blockIdx.y;
@@ -776,7 +776,7 @@ __device__ __forceinline__ bool hwt_node_start(const HwtView &t, uint32_t l, uin
   return false;
 }
 
-__global__ void k_hwt_access(HwtView t, const uint64_t *__restrict__ pos, uint64_t q, uint32_t *__restrict__ out) {
+static __global__ void k_hwt_access(HwtView t, const uint64_t *__restrict__ pos, uint64_t q, uint32_t *__restrict__ out) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= q) return;
   uint64_t i = pos[k];
@@ -797,7 +797,7 @@ __global__ void k_hwt_access(HwtView t, const uint64_t *__restrict__ pos, uint64
   out[k] = res;
 }
 
-__global__ void k_hwt_rank(HwtView t, const uint32_t *__restrict__ sym, const uint64_t *__restrict__ pos, uint64_t q,
+static __global__ void k_hwt_rank(HwtView t, const uint32_t *__restrict__ sym, const uint64_t *__restrict__ pos, uint64_t q,
                            uint64_t *__restrict__ out) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= q) return;

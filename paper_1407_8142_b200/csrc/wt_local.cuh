@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
 
 // Batches: batch b = the rows whose start lies in [b*TW, (b+1)*TW).
 // batch_first[b] = lower_bound(row_start, b*TW), b = 0..nbatch.
-__global__ void k_batches(const uint32_t *__restrict__ row_start, const uint32_t *__restrict__ counts,
+static __global__ void k_batches(const uint32_t *__restrict__ row_start, const uint32_t *__restrict__ counts,
                           uint32_t nbatch, uint32_t *__restrict__ batch_first, uint32_t *__restrict__ bcounts,
                           const uint32_t *err) {
   if (*err) return;
@@ -415,7 +415,7 @@ __global__ void k_batches(const uint32_t *__restrict__ row_start, const uint32_t
 }
 
 // Rows of a local-mode group = the non-empty nodes of level l0 (grid-stride).
-__global__ void k_rows_from_nodes(const uint64_t *__restrict__ level_node_ptr, const uint32_t *__restrict__ ncount,
+static __global__ void k_rows_from_nodes(const uint64_t *__restrict__ level_node_ptr, const uint32_t *__restrict__ ncount,
                                   uint32_t l0, const uint32_t *__restrict__ node_key,
                                   const uint32_t *__restrict__ node_start, uint32_t *__restrict__ row_start,
                                   uint32_t *__restrict__ row_key, uint32_t *__restrict__ counts, const uint32_t *err) {

@@ -23,7 +23,7 @@ namespace wtb {
 // row (non-empty node of level l0, from the node table) split into pieces of
 // <= CH positions.  One CTA of 1024 threads for g >= 1.
 // ---------------------------------------------------------------------------
-__global__ void k_chains_root(uint64_t n, uint64_t CH, uint32_t K, uint32_t *__restrict__ chain_begin,
+static __global__ void k_chains_root(uint64_t n, uint64_t CH, uint32_t K, uint32_t *__restrict__ chain_begin,
                               uint32_t *__restrict__ chain_end, uint32_t *__restrict__ chain_row,
                               uint32_t *__restrict__ row_first, uint32_t *__restrict__ row_start,
                               uint32_t *__restrict__ row_key, uint32_t *__restrict__ counts, const uint32_t *err) {
@@ -45,7 +45,7 @@ __global__ void k_chains_root(uint64_t n, uint64_t CH, uint32_t K, uint32_t *__r
   }
 }
 
-__global__ void __launch_bounds__(1024) k_chains_from_nodes(
+static __global__ void __launch_bounds__(1024) k_chains_from_nodes(
     const uint64_t *__restrict__ level_node_ptr, const uint32_t *__restrict__ ncount, uint32_t l0,
     const uint32_t *__restrict__ node_key, const uint32_t *__restrict__ node_start, uint64_t n, uint64_t CH,
     uint32_t *__restrict__ chain_begin, uint32_t *__restrict__ chain_end, uint32_t *__restrict__ chain_row,
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(512) k_chain_hist(const T *__restrict__ keys, 
 }
 
 // E[d][c] = sum_{c' < c} histT[d][c'] (in place), E[d][nchains] = total; one CTA per digit.
-__global__ void __launch_bounds__(1024) k_chain_scan(uint32_t *__restrict__ histT, uint32_t stride,
+static __global__ void __launch_bounds__(1024) k_chain_scan(uint32_t *__restrict__ histT, uint32_t stride,
                                                     const uint32_t *__restrict__ counts, const uint32_t *err) {
   __shared__ uint32_t shm[33];
   if (*err) return;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(1024) k_chain_scan(uint32_t *__restrict__ hist
 
 // Cseg[r][0..ndig] = exclusive scan over d of the row's digit totals
 // E[d][row_first[r+1]] - E[d][row_first[r]].  One warp per row.
-__global__ void k_row_scan(const uint32_t *__restrict__ E, uint32_t stride, const uint32_t *__restrict__ row_first,
+static __global__ void k_row_scan(const uint32_t *__restrict__ E, uint32_t stride, const uint32_t *__restrict__ row_first,
                            const uint32_t *__restrict__ counts, uint32_t ndig, uint32_t *__restrict__ Cseg,
                            const uint32_t *err) {
   if (*err) return;
@@ -200,7 +200,7 @@ __global__ void k_row_scan(const uint32_t *__restrict__ E, uint32_t stride, cons
 //                      ncount[l0+k] = level total, level_node_ptr
 //   k_row_nodes_emit   writes (key, start) at base + rowoff + local rank
 // ---------------------------------------------------------------------------
-__global__ void k_row_nodes_count(const uint32_t *__restrict__ Cseg, const uint32_t *__restrict__ counts,
+static __global__ void k_row_nodes_count(const uint32_t *__restrict__ Cseg, const uint32_t *__restrict__ counts,
                                   uint32_t tau, uint32_t k_lo, uint32_t nk, uint64_t rstride,
                                   uint32_t *__restrict__ rowcnt, const uint32_t *err) {
   // one warp per (row, level): lanes test 32 prefixes q at a time
@@ -226,7 +226,7 @@ __global__ void k_row_nodes_count(const uint32_t *__restrict__ Cseg, const uint3
 constexpr int SCAN_BLK = 2048;  // rows per scan block
 
 // pass 1: per (level, block) sums.  grid (nblocks, nk), 1024 threads.
-__global__ void __launch_bounds__(1024) k_scan_rows_1(const uint32_t *__restrict__ rowcnt, uint64_t rstride,
+static __global__ void __launch_bounds__(1024) k_scan_rows_1(const uint32_t *__restrict__ rowcnt, uint64_t rstride,
                                                      const uint32_t *__restrict__ counts, uint32_t *__restrict__ bsum,
                                                      uint32_t bstride, const uint32_t *err) {
   __shared__ uint32_t shm[33];
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(1024) k_scan_rows_1(const uint32_t *__restrict
 
 // pass 2: per level, exclusive scan of the block sums (one CTA per level);
 // also the level totals, their CSR bases and level_node_ptr.
-__global__ void __launch_bounds__(1024) k_scan_rows_2(uint32_t *__restrict__ bsum, uint32_t bstride,
+static __global__ void __launch_bounds__(1024) k_scan_rows_2(uint32_t *__restrict__ bsum, uint32_t bstride,
                                                      const uint32_t *__restrict__ counts, uint32_t l0, uint32_t k_lo,
                                                      uint32_t nk, uint32_t L, uint32_t *__restrict__ ncount,
                                                      uint64_t *__restrict__ level_node_ptr, const uint32_t *err) {
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(1024) k_scan_rows_2(uint32_t *__restrict__ bsu
 }
 
 // Level CSR bases: level_node_ptr[lev] for the group's levels (runs after pass 2).
-__global__ void k_level_ptr(const uint32_t *__restrict__ ncount, uint32_t l0, uint32_t k_lo, uint32_t nk, uint32_t L,
+static __global__ void k_level_ptr(const uint32_t *__restrict__ ncount, uint32_t l0, uint32_t k_lo, uint32_t nk, uint32_t L,
                             uint64_t *__restrict__ level_node_ptr, const uint32_t *err) {
   if (*err) return;
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -281,7 +281,7 @@ __global__ void k_level_ptr(const uint32_t *__restrict__ ncount, uint32_t l0, ui
 }
 
 // pass 3: rowoff[k][r] = exclusive prefix within the level (in place over rowcnt).
-__global__ void __launch_bounds__(1024) k_scan_rows_3(uint32_t *__restrict__ rowcnt, uint64_t rstride,
+static __global__ void __launch_bounds__(1024) k_scan_rows_3(uint32_t *__restrict__ rowcnt, uint64_t rstride,
                                                      const uint32_t *__restrict__ counts,
                                                      const uint32_t *__restrict__ bsum, uint32_t bstride,
                                                      const uint32_t *err) {
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(1024) k_scan_rows_3(uint32_t *__restrict__ row
   }
 }
 
-__global__ void k_row_nodes_emit(const uint32_t *__restrict__ Cseg, const uint32_t *__restrict__ counts, uint32_t tau,
+static __global__ void k_row_nodes_emit(const uint32_t *__restrict__ Cseg, const uint32_t *__restrict__ counts, uint32_t tau,
                                  uint32_t l0, uint32_t k_lo, uint32_t nk, uint64_t rstride,
                                  const uint32_t *__restrict__ rowoff, const uint64_t *__restrict__ level_node_ptr,
                                  const uint32_t *__restrict__ row_key, const uint32_t *__restrict__ row_start,

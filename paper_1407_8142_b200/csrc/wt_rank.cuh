@@ -13,7 +13,7 @@ namespace wtb {
 // A7 finalize: rank_block (u16, relative to the superblock) and rank_super.
 // k_rank_local: one warp per (level, superblock); k_rank_super: one CTA per level.
 // ---------------------------------------------------------------------------
-__global__ void k_rank_local(const uint64_t *__restrict__ bits, uint64_t wpl, uint64_t bpl, uint64_t nsup_data,
+static __global__ void k_rank_local(const uint64_t *__restrict__ bits, uint64_t wpl, uint64_t bpl, uint64_t nsup_data,
                              uint32_t lbeg, uint32_t nl, uint16_t *__restrict__ rank_block,
                              uint64_t *__restrict__ suptot, const uint32_t *err) {
   // One warp per (level, superblock) of levels [lbeg, lbeg+nl): popcount of its
@@ -54,7 +54,7 @@ __global__ void k_rank_local(const uint64_t *__restrict__ bits, uint64_t wpl, ui
   if (lane == 31) suptot[(uint64_t)l * nsup_data + s] = incl;
 }
 
-__global__ void __launch_bounds__(1024) k_rank_super(const uint64_t *__restrict__ suptot, uint64_t nsup_data,
+static __global__ void __launch_bounds__(1024) k_rank_super(const uint64_t *__restrict__ suptot, uint64_t nsup_data,
                                                     uint64_t spl, uint64_t *__restrict__ rank_super,
                                                     const uint32_t *err) {
   __shared__ unsigned long long warp_tot[33];
@@ -112,7 +112,7 @@ __device__ __forceinline__ uint64_t d_rank1(const TreeView &t, uint32_t l, uint6
   return r;
 }
 
-__global__ void k_access(TreeView t, const uint64_t *__restrict__ pos, uint64_t q, uint32_t *__restrict__ out) {
+static __global__ void k_access(TreeView t, const uint64_t *__restrict__ pos, uint64_t q, uint32_t *__restrict__ out) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= q) return;
   uint64_t i = pos[k];
@@ -130,7 +130,7 @@ __global__ void k_access(TreeView t, const uint64_t *__restrict__ pos, uint64_t 
   out[k] = sym;
 }
 
-__global__ void k_rank_query(TreeView t, uint64_t sigma, const uint32_t *__restrict__ sym,
+static __global__ void k_rank_query(TreeView t, uint64_t sigma, const uint32_t *__restrict__ sym,
                              const uint64_t *__restrict__ pos, uint64_t q, uint64_t *__restrict__ out) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= q) return;

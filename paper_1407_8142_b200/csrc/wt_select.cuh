@@ -19,7 +19,7 @@ namespace wtb {
 
 constexpr uint32_t SEL_SAMPLE = 4096;
 
-__global__ void k_fill_u32(uint32_t *__restrict__ a, uint64_t cnt, uint32_t v) {
+static __global__ void k_fill_u32(uint32_t *__restrict__ a, uint64_t cnt, uint32_t v) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x)
     a[i] = v;
 }
@@ -37,7 +37,7 @@ __device__ __forceinline__ uint32_t select_in_word(uint64_t w, uint32_t j) {
   return 32 + __fns((uint32_t)(w >> 32), 0, (int)(j - plo) + 1);
 }
 
-__global__ void k_select_dir(TreeView t, uint32_t *__restrict__ sel0, uint32_t *__restrict__ sel1, uint64_t sps) {
+static __global__ void k_select_dir(TreeView t, uint32_t *__restrict__ sel0, uint32_t *__restrict__ sel1, uint64_t sps) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (uint64_t)t.L * t.bpl) return;
   const uint32_t l = (uint32_t)(gid / t.bpl);
@@ -78,7 +78,7 @@ __global__ void k_select_dir(TreeView t, uint32_t *__restrict__ sel0, uint32_t *
 }
 
 // position of the k'th (1-based) b-bit of level l, or n
-__device__ uint64_t d_select_b(const TreeView &t, const uint32_t *sel, uint64_t sps, uint32_t l, uint32_t b,
+static __device__ uint64_t d_select_b(const TreeView &t, const uint32_t *sel, uint64_t sps, uint32_t l, uint32_t b,
                                uint64_t k) {
   if (k == 0) return t.n;
   const uint64_t j = (k - 1) / SEL_SAMPLE;
@@ -115,7 +115,7 @@ __device__ __forceinline__ uint64_t d_rank_b(const TreeView &t, uint32_t l, uint
 }
 
 // tree: top-down node ranges of c's prefix, then bottom-up selects
-__global__ void k_wt_select(TreeView t, const uint32_t *__restrict__ sel0, const uint32_t *__restrict__ sel1,
+static __global__ void k_wt_select(TreeView t, const uint32_t *__restrict__ sel0, const uint32_t *__restrict__ sel1,
                             uint64_t sps, uint64_t sigma, const uint32_t *__restrict__ sym,
                             const uint64_t *__restrict__ kk, uint64_t q, uint64_t *__restrict__ out) {
   const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -143,7 +143,7 @@ __global__ void k_wt_select(TreeView t, const uint32_t *__restrict__ sel0, const
 }
 
 // matrix: class starts top-down, then bottom-up selects
-__global__ void k_wm_select(TreeView t, const uint64_t *__restrict__ zeros, const uint32_t *__restrict__ sel0,
+static __global__ void k_wm_select(TreeView t, const uint64_t *__restrict__ zeros, const uint32_t *__restrict__ sel0,
                             const uint32_t *__restrict__ sel1, uint64_t sps, uint64_t sigma,
                             const uint32_t *__restrict__ sym, const uint64_t *__restrict__ kk, uint64_t q,
                             uint64_t *__restrict__ out) {

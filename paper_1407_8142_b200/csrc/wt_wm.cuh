@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(WPB * 32, 4) k_wm_group4(GroupParams p) {
 }
 
 // zeros[l] = n - (ones of level l), from the rank directory's level totals.
-__global__ void k_wm_zeros(const uint64_t *__restrict__ rank_super, uint64_t spl, uint32_t L, uint64_t n,
+static __global__ void k_wm_zeros(const uint64_t *__restrict__ rank_super, uint64_t spl, uint32_t L, uint64_t n,
                            uint64_t *__restrict__ zeros, const uint32_t *err) {
   if (*err) return;
   const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
@@ -632,7 +632,7 @@ __global__ void k_wm_zeros(const uint64_t *__restrict__ rank_super, uint64_t spl
 
 // Batched queries: a 0 bit at level l maps i -> rank0(i),
 // a 1 bit maps i -> zeros[l] + rank1(i).
-__global__ void k_wm_access(TreeView t, const uint64_t *__restrict__ zeros, const uint64_t *__restrict__ pos,
+static __global__ void k_wm_access(TreeView t, const uint64_t *__restrict__ zeros, const uint64_t *__restrict__ pos,
                             uint64_t q, uint32_t *__restrict__ out) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= q) return;
@@ -648,7 +648,7 @@ __global__ void k_wm_access(TreeView t, const uint64_t *__restrict__ zeros, cons
   out[k] = sym;
 }
 
-__global__ void k_wm_rank(TreeView t, const uint64_t *__restrict__ zeros, uint64_t sigma,
+static __global__ void k_wm_rank(TreeView t, const uint64_t *__restrict__ zeros, uint64_t sigma,
                           const uint32_t *__restrict__ sym, const uint64_t *__restrict__ pos, uint64_t q,
                           uint64_t *__restrict__ out) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
