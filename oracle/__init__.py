@@ -149,6 +149,8 @@ def _load():
             lib.oracle_hwt_access.restype = ctypes.c_uint32
             lib.oracle_hwt_rank.argtypes = [ctypes.POINTER(_HWT), ctypes.c_uint32, ctypes.c_uint64]
             lib.oracle_hwt_rank.restype = ctypes.c_uint64
+            lib.oracle_hwt_select.argtypes = [ctypes.POINTER(_HWT), ctypes.c_uint32, ctypes.c_uint64]
+            lib.oracle_hwt_select.restype = ctypes.c_uint64
             _lib = lib
     return _lib
 
@@ -409,6 +411,10 @@ class OracleHWT:
     def rank(self, symbols, positions) -> np.ndarray:
         return np.array([self._lib.oracle_hwt_rank(self._t, int(c), int(i))
                          for c, i in zip(symbols, positions)], dtype=np.uint64)
+
+    def select(self, symbols, ks) -> np.ndarray:
+        return np.array([self._lib.oracle_hwt_select(self._t, int(c), int(k))
+                         for c, k in zip(symbols, ks)], dtype=np.uint64)
 
     def close(self):
         if getattr(self, "_t", None):

@@ -1019,3 +1019,42 @@ uint64_t oracle_hwt_rank(const oracle_hwt *t, uint32_t c, uint64_t i) {
   (void)e;
   return r;
 }
+
+/* select_c(S, k) on the Huffman-shaped tree (PAPER.md:207-208 with the tree
+ * walk of :204-206): descend along c's code to find the node of every level,
+ * then climb from the deepest node -- the k'th occurrence of c is the k'th
+ * bit equal to c's last code bit inside that node, and at every level above
+ * the r'th position of the child is the r'th bit equal to the level's code
+ * bit inside the parent.  Bits are found by a plain scan of the level. */
+static uint64_t hwt_select_bit(const oracle_hwt *t, uint32_t l, uint64_t s, uint64_t e, uint32_t b, uint64_t j) {
+  const uint64_t *B = t->bits + t->level_word_ptr[l];
+  for (uint64_t i = s; i < e; i++) {
+    if ((uint32_t)((B[i >> 6] >> (i & 63)) & 1u) == b) {
+      if (--j == 0) return i;
+    }
+  }
+  return UINT64_MAX;
+}
+
+uint64_t oracle_hwt_select(const oracle_hwt *t, uint32_t c, uint64_t k) {
+  if (!t || (uint64_t)c >= t->sigma || k == 0) return UINT64_MAX;
+  if (t->levels == 0) return (t->n && c == t->only_symbol && k <= t->n) ? k - 1 : UINT64_MAX;
+  uint32_t L = t->code_len[c];
+  if (L == 0) return UINT64_MAX;
+  uint64_t s[64], e[64];
+  s[0] = 0;
+  e[0] = t->level_len[0];
+  uint32_t p = 0;
+  for (uint32_t l = 0; l + 1 < L; l++) {
+    p = 2 * p + ((t->code[c] >> (L - 1 - l)) & 1u);
+    if (!hwt_node(t, l + 1, p, &s[l + 1], &e[l + 1])) return UINT64_MAX;
+  }
+  uint64_t r = k;  /* 1-based rank inside the node of level l */
+  for (int l = (int)L - 1; l >= 0; l--) {
+    uint32_t b = (t->code[c] >> (L - 1 - (uint32_t)l)) & 1u;
+    uint64_t pos = hwt_select_bit(t, (uint32_t)l, s[l], e[l], b, r);
+    if (pos == UINT64_MAX) return UINT64_MAX;
+    r = pos - s[l] + 1;
+  }
+  return r - 1;
+}

@@ -116,6 +116,17 @@ def _queries(S, sigma, t, k=200, seed=0):
     assert t.access([n])[0] == 0xFFFFFFFF
     assert t.rank([0], [n])[0] == 2**64 - 1
     assert t.rank([sigma], [0])[0] == 2**64 - 1
+    # select_c(k): the k'th occurrence by brute force; k = 0 / too large / c >= sigma -> UINT64_MAX
+    S = np.asarray(S)
+    cs = rng.integers(0, sigma, size=k // 4)
+    cs[: min(len(cs), 50)] = S[rng.integers(0, n, size=min(len(cs), 50))]
+    ks = rng.integers(0, 20, size=cs.size)
+    exp = []
+    for c, kk in zip(cs, ks):
+        occ = np.nonzero(S == c)[0]
+        exp.append(int(occ[kk - 1]) if 1 <= kk <= occ.size else 2**64 - 1)
+    assert t.select(cs, ks).tolist() == exp
+    assert t.select([sigma], [1])[0] == 2**64 - 1
 
 
 @pytest.mark.parametrize("fname", sorted(os.listdir(GOLDEN)))
@@ -150,6 +161,10 @@ def test_hwt_golden(fname):
             ci, v = item.split(":")
             c, i = map(int, ci.split("@"))
             assert t.rank([c], [i])[0] == int(v)
+        for item in g.get("select", "").split():
+            ck, v = item.split(":")
+            c, kk = map(int, ck.split("#"))
+            assert t.select([c], [kk])[0] == int(v)
     check_hwt(S, sigma, o)
 
 
@@ -178,6 +193,11 @@ def test_hwt_exhaustive_tiny():
                         assert t.access([i])[0] == S[i]
                         for c in range(sigma):
                             assert t.rank([c], [i])[0] == pins.rank_bruteforce(S, c, i)
+                    for c in range(sigma):
+                        occ = np.nonzero(S == c)[0]
+                        for kk in range(0, n + 2):
+                            want = int(occ[kk - 1]) if 1 <= kk <= occ.size else 2**64 - 1
+                            assert t.select([c], [kk])[0] == want
                 cnt += 1
     assert cnt > 1000
 
@@ -215,6 +235,7 @@ def test_hwt_degenerate():
     with oracle.OracleHWT(S, 5) as t:
         assert t.access([0, 999]).tolist() == [3, 3]
         assert t.rank([3, 0, 4], [10, 10, 999]).tolist() == [11, 0, 0]
+        assert t.select([3, 3, 3, 0], [1, 1000, 1001, 1]).tolist() == [0, 999, 2**64 - 1, 2**64 - 1]
     # two symbols: one level, the bitmap is the sequence (0 -> code 0 by R-18)
     S = np.array([1, 0, 1, 1, 0], np.uint8)
     o = check_hwt(S, 2)
