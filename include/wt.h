@@ -264,6 +264,13 @@ int hwt_free(hwt_tree *t);
 int hwt_access(const hwt_tree *t, const uint64_t *d_pos, uint64_t q, uint32_t *d_out, void *stream);
 int hwt_rank(const hwt_tree *t, const uint32_t *d_sym, const uint64_t *d_pos, uint64_t q,
              uint64_t *d_out, void *stream);
+/* hwt_select -- batched select_c(S, k): descent along c's
+ * code to the deepest node, then bit selects climbing back up (binary
+ * searches over each level's rank directory; no select index is needed).
+ * Buffers, sentinels (UINT64_MAX for k == 0, k > count of c, c >= sigma or
+ * c absent) and errors as wt_select. */
+int hwt_select(const hwt_tree *t, const uint32_t *d_sym, const uint64_t *d_k, uint64_t q, uint64_t *d_out,
+               void *stream);
 
 /* ---- sharded build helpers (orchestrated by the Python
  * module paper_1407_8142_b200/dist.py over torch.distributed / NCCL) ----

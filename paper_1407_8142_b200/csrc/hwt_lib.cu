@@ -394,5 +394,14 @@ int hwt_rank(const hwt_tree *t, const uint32_t *d_sym, const uint64_t *d_pos, ui
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
 }
 
+int hwt_select(const hwt_tree *t, const uint32_t *d_sym, const uint64_t *d_k, uint64_t q, uint64_t *d_out,
+               void *stream) {
+  if (!t || !t->internal || (q > 0 && (!d_sym || !d_k || !d_out))) return WT_EINVAL;
+  if (q == 0) return WT_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k_hwt_select<<<(unsigned)((q + 127) / 128), 128, 0, s>>>(view_of_hwt(t), d_sym, d_k, q, d_out);
+  return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
+}
+
 }  // extern "C"
 

@@ -821,4 +821,104 @@ static __global__ void k_hwt_rank(HwtView t, const uint32_t *__restrict__ sym, c
   out[k] = r;
 }
 
+// select_c on the Huffman-shaped tree: descend along c's
+// code for the node of every level, then climb from the deepest node with
+// select_b inside each node; select_b by binary searches over the level's
+// superblocks, blocks and words (no select directory for ragged levels).
+__device__ __forceinline__ uint32_t hwt_select_in_word(uint64_t v, uint32_t r) {  // r'th (0-based) set bit
+  for (uint32_t i = 0; i < r; i++) v &= v - 1;
+  return (uint32_t)__ffsll((long long)v) - 1u;
+}
+
+// position of the T'th (1-based) b-bit of level l, or UINT64_MAX
+__device__ __forceinline__ uint64_t hwt_select_b(const HwtView &t, uint32_t l, uint32_t b, uint64_t T) {
+  const uint64_t nl = t.level_len[l];
+  const uint64_t nsd = t.sptr[l + 1] - t.sptr[l] - 1;  // superblocks holding data
+  const uint64_t *sup = t.rank_super + t.sptr[l];
+  const uint16_t *blk = t.rank_block + t.bptr[l];
+  const uint64_t *B = t.bits + t.wptr[l];
+  auto before_sup = [&](uint64_t i) -> uint64_t {  // b-bits in [0, min(i*65536, nl))
+    const uint64_t p = i * 65536 < nl ? i * 65536 : nl;
+    return b ? sup[i] : p - sup[i];
+  };
+  if (T == 0 || before_sup(nsd) < T) return ~0ull;
+  uint64_t lo = 0, hi = nsd;  // last superblock with before < T
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (before_sup(mid) < T) lo = mid; else hi = mid;
+  }
+  const uint64_t base_s = before_sup(lo);
+  const uint64_t nblk = t.bptr[l + 1] - t.bptr[l];
+  uint64_t blo = lo * 128, bhi = (lo * 128 + 128 < nblk ? lo * 128 + 128 : nblk);
+  auto before_blk = [&](uint64_t j) -> uint64_t {
+    const uint64_t ones = blk[j];
+    return base_s + (b ? ones : (j * 512 - lo * 65536) - ones);
+  };
+  while (bhi - blo > 1) {
+    const uint64_t mid = (blo + bhi) >> 1;
+    if (before_blk(mid) < T) blo = mid; else bhi = mid;
+  }
+  uint64_t need = T - 1 - before_blk(blo);
+  for (int i = 0; i < 8; i++) {
+    const uint64_t base = blo * 512 + i * 64;
+    if (base >= nl) break;
+    uint64_t v = b ? B[blo * 8 + i] : ~B[blo * 8 + i];
+    if (base + 64 > nl) v &= (1ull << (nl - base)) - 1ull;
+    const uint32_t pc = __popcll(v);
+    if (need < pc) return base + hwt_select_in_word(v, (uint32_t)need);
+    need -= pc;
+  }
+  return ~0ull;
+}
+
+__device__ __forceinline__ uint64_t hwt_rank_b(const HwtView &t, uint32_t l, uint64_t i, uint32_t b) {
+  const uint64_t r1 = hwt_rank1(t, l, i);
+  return b ? r1 : i - r1;
+}
+
+static __global__ void k_hwt_select(HwtView t, const uint32_t *__restrict__ sym, const uint64_t *__restrict__ kk,
+                                    uint64_t q, uint64_t *__restrict__ out) {
+  const uint64_t qi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= q) return;
+  const uint32_t c = sym[qi];
+  const uint64_t K = kk[qi];
+  uint64_t res = ~0ull;
+  if ((uint64_t)c < t.sigma && K > 0) {
+    if (t.h == 0) {
+      if (t.n && c == t.only_symbol && K <= t.n) res = K - 1;
+    } else if (t.code_len[c]) {
+      const uint32_t L = t.code_len[c], cd = t.code[c];
+      uint64_t st[HUFF_MAXLEN];
+      st[0] = 0;
+      uint32_t p = 0;
+      bool ok = true;
+      for (uint32_t l = 0; l + 1 < L && ok; l++) {
+        p = 2 * p + ((cd >> (L - 1 - l)) & 1u);
+        ok = hwt_node_start(t, l + 1, p, &st[l + 1]);
+      }
+      if (ok) {
+        uint64_t r = K;  // 1-based rank inside the node of level l
+        for (int l = (int)L - 1; l >= 0 && r != ~0ull; l--) {
+          const uint32_t b = (cd >> (L - 1 - (uint32_t)l)) & 1u;
+          const uint64_t pos = hwt_select_b(t, (uint32_t)l, b, hwt_rank_b(t, (uint32_t)l, st[l], b) + r);
+          // the answer must lie inside the node: its b-bits before pos, counted from the node start, are r - 1
+          r = pos == ~0ull ? ~0ull : pos - st[l] + 1;
+          if (r != ~0ull && l == (int)L - 1) {
+            // node end at the deepest level: the next node's start (or the level end)
+            uint64_t a = t.node_ptr[l], z = t.node_ptr[l + 1], e = t.level_len[l];
+            while (a < z) {
+              const uint64_t mid = (a + z) >> 1;
+              if (t.node_key[mid] <= p) a = mid + 1; else z = mid;
+            }
+            if (a < t.node_ptr[l + 1]) e = t.node_start[a];
+            if (pos >= e) r = ~0ull;
+          }
+        }
+        if (r != ~0ull) res = r - 1;
+      }
+    }
+  }
+  out[qi] = res;
+}
+
 }  // namespace wtb

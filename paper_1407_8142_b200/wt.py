@@ -463,6 +463,9 @@ def _load_hwt():
     lib.hwt_rank.argtypes = [PH, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                              ctypes.c_void_p]
     lib.hwt_rank.restype = ctypes.c_int
+    lib.hwt_select.argtypes = [PH, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                               ctypes.c_void_p]
+    lib.hwt_select.restype = ctypes.c_int
     lib._hwt_ready = True
     return lib
 
@@ -534,6 +537,22 @@ class HuffmanWaveletTree:
                           ctypes.c_void_p(_stream_ptr(stream)))
         if rc != WT_OK:
             raise WtError(rc, "hwt_rank")
+        return out.view(torch.uint64)
+
+    def select(self, sym: torch.Tensor, k: torch.Tensor, stream=None) -> torch.Tensor:
+        """hwt_select: position of the k'th (1-based) occurrence of each symbol."""
+        lib = _load_hwt()
+        sym = sym.contiguous().view(-1)
+        k = k.contiguous().view(-1)
+        if sym.numel() != k.numel():
+            raise ValueError("sym and k must have the same length")
+        out = torch.empty(k.numel(), dtype=torch.int64, device=k.device)
+        rc = lib.hwt_select(self.handle, ctypes.c_void_p(sym.data_ptr() if sym.numel() else 0),
+                            ctypes.c_void_p(k.data_ptr() if k.numel() else 0), k.numel(),
+                            ctypes.c_void_p(out.data_ptr() if out.numel() else 0),
+                            ctypes.c_void_p(_stream_ptr(stream)))
+        if rc != WT_OK:
+            raise WtError(rc, "hwt_select")
         return out.view(torch.uint64)
 
     def free(self):

@@ -21,7 +21,7 @@ def test_header_declares_expected_calls():
     names = _declared()
     for req in ("wt_build", "wt_build_host", "wt_free", "wt_access", "wt_rank",
                 "wm_build", "wm_free", "wm_access", "wm_rank",
-                "hwt_build", "hwt_free", "hwt_access", "hwt_rank", "wt_digit_counts", "wt_digits",
+                "hwt_build", "hwt_free", "hwt_access", "hwt_rank", "hwt_select", "wt_digit_counts", "wt_digits",
                 "wt_partition", "wt_gather_bits", "wt_create", "wt_finish"):
         assert req in names
 

@@ -52,6 +52,19 @@ def _queries(t, S, sigma, k=3000, seed=0):
     rk = t.rank(torch.from_numpy(sym.view(np.int32)).cuda(), torch.from_numpy(pos.astype(np.int64)).cuda()).cpu().numpy()
     assert np.array_equal(acc, want_a)
     assert np.array_equal(rk, want_r)
+    # select_c(k): symbols from S and random ones, k in [0, count + 1]
+    cs = np.where(rng.random(k) < 0.7, S[rng.integers(0, max(n, 1), k)] if n else 0,
+                  rng.integers(0, sigma + 2, k)).astype(np.uint32)
+    cnt = np.bincount(S.astype(np.int64), minlength=sigma + 2) if n else np.zeros(sigma + 2, np.int64)
+    ks = (rng.random(k) * (cnt[np.minimum(cs, sigma + 1)] + 2)).astype(np.int64)
+    # expected: the k'th occurrence from a stable sort of S (brute force, no oracle walk)
+    order = np.argsort(S, kind="stable") if n else np.zeros(0, np.int64)
+    first = np.searchsorted(S[order], cs) if n else np.zeros(k, np.int64)
+    c_ok = (cs < sigma) & (ks >= 1) & (ks <= cnt[np.minimum(cs, sigma + 1)])
+    want_s = np.full(k, 2**64 - 1, dtype=np.uint64)
+    want_s[c_ok] = order[first[c_ok] + ks[c_ok] - 1]
+    sel = t.select(torch.from_numpy(cs.view(np.int32)).cuda(), torch.from_numpy(ks).cuda()).cpu().numpy()
+    assert np.array_equal(sel, want_s)
     ok = pos < n
     if n:
         assert np.array_equal(acc[ok], S[pos[ok]].astype(np.uint32))
@@ -157,3 +170,18 @@ def test_hwt_unaligned_device_pointer(dtype, sigma):
         for k in KEYS:
             assert np.array_equal(got[k], want[k]), (off, k)
         t.free()
+
+
+@pytest.mark.parametrize("sigma,n", [(5, 3000), (256, 5000), (3000, 4000), (1, 100)])
+def test_hwt_select_vs_oracle(sigma, n):
+    S = np.minimum(np.random.default_rng(n).zipf(1.4, n) - 1, sigma - 1).astype(np.uint16)
+    import paper_1407_8142_b200 as wt
+    t = wt.hwt_build(torch.from_numpy(S).cuda(), sigma)
+    rng = np.random.default_rng(1)
+    cs = np.concatenate([S[rng.integers(0, n, 400)], rng.integers(0, sigma + 1, 100)]).astype(np.uint32)
+    ks = rng.integers(0, 60, cs.size).astype(np.int64)
+    with oracle.OracleHWT(S, sigma) as o:
+        want = o.select(cs, ks)
+    got = t.select(torch.from_numpy(cs.view(np.int32)).cuda(), torch.from_numpy(ks).cuda()).cpu().numpy()
+    assert np.array_equal(got, want)
+    t.free()
