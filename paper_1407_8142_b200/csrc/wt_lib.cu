@@ -12,6 +12,8 @@
 #include "wt_prep.cuh"
 #include "wt_rank.cuh"
 #include "wt_select.cuh"
+#include "wt_small.cuh"
+#include "wt_dist.cuh"
 
 using namespace wtb;
 using namespace wthost;
@@ -212,7 +214,10 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   }
 
   // ---- plan: groups of <= 8 levels ----
-  const uint32_t NG = (L + TAU_MAX - 1) / TAU_MAX;
+  // one or two levels (sigma <= 4): the direct kernels of wt_small.cuh
+  const bool small = (L == 1 || L == 2) && n > 0 && eb == 1 && !getenv("WT_NO_SMALL") &&
+                     (from_host || reinterpret_cast<uintptr_t>(d_seq) % 16 == 0);
+  const uint32_t NG = small ? 0u : (L + TAU_MAX - 1) / TAU_MAX;
   GroupBufs G[4];
   for (uint32_t g = 0; g < NG; g++) {
     GroupBufs &gb = G[g];
@@ -259,6 +264,9 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   uint32_t *err = A.alloc<uint32_t>(4, false);
   uint32_t *ncount = A.alloc<uint32_t>(L + 1, false);
   uint64_t *suptot = A.alloc<uint64_t>(L * NSD, false);
+  const uint32_t small_tiles = small ? (uint32_t)((n + SMALL_TILE - 1) / SMALL_TILE) : 0u;
+  uint32_t *small_zc = small ? A.alloc<uint32_t>(small_tiles, false) : nullptr;
+  uint64_t *small_tot = small ? A.alloc<uint64_t>(1, false) : nullptr;
 
   // pinned staging for the single D2H; one per host thread, so that builds
   // issued concurrently from several threads do not share it
@@ -302,6 +310,27 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     rec.end();
     side_used = true;
   };
+
+  if (small) {
+    // ---- sigma <= 4: level 0 by ballots, level 1 as two compacted bit streams ----
+    rec.begin("k_small_count", n * eb);
+    k_small_count<<<small_tiles, SMALL_WARPS * 32, 0, s>>>((const uint8_t *)seq, n, (uint32_t)sigma, L - 1,
+                                                           small_zc, err);
+    k_part_scan<<<1, 1024, 0, s>>>(small_zc, small_tiles, small_tot);
+    chk(cudaGetLastError());
+    rec.end();
+    rec.begin("k_small_write", n * eb + (uint64_t)L * n / 8);
+    k_small_write<<<small_tiles, SMALL_WARPS * 32, 0, s>>>((const uint8_t *)seq, n, L, small_zc, small_tot, t->bits,
+                                                           WPL);
+    k_small_nodes<<<1, 32, 0, s>>>(L, n, small_tot, t->level_node_ptr, t->node_key, t->node_start);
+    chk(cudaGetLastError());
+    rec.end();
+    rec.begin("k_rank_local", (uint64_t)L * (WPL * 8 + BPL * 2 + NSD * 8));
+    k_rank_local<<<(unsigned)(((uint64_t)L * NSD * 32 + 255) / 256), 256, 0, s>>>(t->bits, WPL, BPL, NSD, 0, L,
+                                                                                     t->rank_block, suptot, err);
+    chk(cudaGetLastError());
+    rec.end();
+  }
 
   const void *keys_in = seq;
   for (uint32_t g = 0; g < NG || (g == 0 && L == 0); g++) {
