@@ -137,13 +137,39 @@ inline void configure_pool_once() {
 }
 
 // Stream-ordered allocations that are released together on error.
+// Per-thread scratch arena: reused by consecutive builds of one host thread
+// (every build synchronises its stream before returning), so that a small
+// build makes no allocation calls for its scratch.  Capped at ARENA_MAX;
+// larger needs fall back to stream-ordered allocations.
+struct Arena {
+  char *base = nullptr;
+  size_t cap = 0, used = 0, want = 0;
+  bool busy = false;
+};
+inline Arena &thread_arena() {
+  static thread_local Arena a;
+  return a;
+}
+constexpr size_t ARENA_MAX = 64ull << 20;
+
+// Stream-ordered allocations that are released together on error.
 struct Allocs {
   cudaStream_t s;
   std::vector<void *> scratch, outputs;
   bool fail = false;
+  Arena *ar = nullptr;  // scratch is carved from the thread's arena while set
   template <typename T>
   T *alloc(size_t count, bool output) {
     if (count == 0) count = 1;
+    const size_t bytes = (count * sizeof(T) + 255) & ~(size_t)255;
+    if (!output && ar) {
+      ar->want += bytes;
+      if (ar->used + bytes <= ar->cap) {
+        void *p = ar->base + ar->used;
+        ar->used += bytes;
+        return static_cast<T *>(p);
+      }
+    }
     void *p = nullptr;
     if (cudaMallocAsync(&p, count * sizeof(T), s) != cudaSuccess) {
       fail = true;
@@ -152,6 +178,31 @@ struct Allocs {
     (output ? outputs : scratch).push_back(p);
     return static_cast<T *>(p);
   }
+  // several outputs in one allocation (released together by the owner's free)
+  bool alloc_outputs(std::initializer_list<std::pair<void **, size_t>> items) {
+    size_t total = 0;
+    for (const auto &it : items) total += (it.second + 255) & ~(size_t)255;
+    void *p = nullptr;
+    if (cudaMallocAsync(&p, total ? total : 256, s) != cudaSuccess) {
+      fail = true;
+      for (const auto &it : items) *it.first = nullptr;
+      return false;
+    }
+    outputs.push_back(p);
+    char *c = static_cast<char *>(p);
+    for (const auto &it : items) {
+      *it.first = c;
+      c += (it.second + 255) & ~(size_t)255;
+    }
+    return true;
+  }
+  void use_arena() {  // not for nested builds (the arena is then busy)
+    Arena &a = thread_arena();
+    if (a.busy) return;
+    a.busy = true;
+    a.used = a.want = 0;
+    ar = &a;
+  }
   void free_scratch() {
     for (void *p : scratch) cudaFreeAsync(p, s);
     scratch.clear();
@@ -159,6 +210,18 @@ struct Allocs {
   void free_outputs() {
     for (void *p : outputs) cudaFreeAsync(p, s);
     outputs.clear();
+  }
+  // after the build's stream is synchronised: release (and grow) the arena
+  ~Allocs() {
+    if (!ar) return;
+    if (ar->want > ar->cap && ar->want <= ARENA_MAX) {
+      if (ar->base) cudaFree(ar->base);
+      ar->base = nullptr;
+      ar->cap = 0;
+      if (cudaMalloc(&ar->base, ar->want) == cudaSuccess) ar->cap = ar->want;
+    }
+    ar->used = 0;
+    ar->busy = false;
   }
 };
 

@@ -197,12 +197,10 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   t->words_per_level = WPL;
   t->blocks_per_level = BPL;
   t->supers_per_level = SPL;
-  t->bits = A.alloc<uint64_t>(L * WPL, true);
-  t->level_node_ptr = A.alloc<uint64_t>(L + 1, true);
-  t->node_key = A.alloc<uint32_t>(max_nodes, true);
-  t->node_start = A.alloc<uint32_t>(max_nodes, true);
-  t->rank_block = A.alloc<uint16_t>(L * BPL, true);
-  t->rank_super = A.alloc<uint64_t>(L * SPL, true);
+  A.use_arena();
+  A.alloc_outputs({{(void **)&t->bits, L * WPL * 8}, {(void **)&t->level_node_ptr, (L + 1) * 8},
+                   {(void **)&t->node_key, max_nodes * 4}, {(void **)&t->node_start, max_nodes * 4},
+                   {(void **)&t->rank_block, L * BPL * 2}, {(void **)&t->rank_super, L * SPL * 8}});
 
   const void *seq = d_seq;
   if (from_host) {
