@@ -293,20 +293,25 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   cudaStream_t side = side_stream();
   cudaEvent_t ev_side = nullptr;
   bool side_used = false;
+  // (the last group's directory has no later pass to overlap: main stream)
   auto rank_levels = [&](uint32_t lbeg, uint32_t nl) {
     if (!NSD || !nl || !n) return;
-    cudaEvent_t ev;
-    chk(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    chk(cudaEventRecord(ev, s));
-    chk(cudaStreamWaitEvent(side, ev, 0));
-    cudaEventDestroy(ev);
+    const bool last = lbeg + nl >= L;
+    cudaStream_t rs = last ? s : side;
+    if (!last) {
+      cudaEvent_t ev;
+      chk(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      chk(cudaEventRecord(ev, s));
+      chk(cudaStreamWaitEvent(side, ev, 0));
+      cudaEventDestroy(ev);
+      side_used = true;
+    }
     const uint64_t warps = (uint64_t)nl * NSD;
-    rec.begin("k_rank_local", nl * WPL * 8 + nl * BPL * 2 + nl * NSD * 8, side);
-    k_rank_local<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, side>>>(t->bits, WPL, BPL, NSD, lbeg, nl,
-                                                                           t->rank_block, suptot, err);
+    rec.begin("k_rank_local", nl * WPL * 8 + nl * BPL * 2 + nl * NSD * 8, rs);
+    k_rank_local<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, rs>>>(t->bits, WPL, BPL, NSD, lbeg, nl,
+                                                                         t->rank_block, suptot, err);
     chk(cudaGetLastError());
     rec.end();
-    side_used = true;
   };
 
   if (small) {

@@ -184,9 +184,33 @@ class _SelectOps:
         return out.view(torch.uint64)
 
 
+class _Lazy:
+    """A zero-copy torch view of one library array, made on first access
+    (building a tree does not pay for views it never uses)."""
+
+    def __init__(self, field, count, typestr, dtype):
+        self.field, self.count, self.typestr, self.dtype = field, count, typestr, dtype
+
+    def __set_name__(self, owner, name):
+        self.name = name
+
+    def __get__(self, obj, cls=None):
+        if obj is None:
+            return self
+        v = _view(getattr(obj.handle.contents, self.field), self.count(obj), self.typestr, self.dtype, obj.device)
+        obj.__dict__[self.name] = v
+        return v
+
+
 class WaveletTree(_SelectOps):
     """A built tree.  Arrays are zero-copy torch views of library memory and
     stay valid until ``free()`` (called on garbage collection too)."""
+    bits = _Lazy("bits", lambda o: o.levels * o.words_per_level, "<u8", torch.uint64)
+    level_node_ptr = _Lazy("level_node_ptr", lambda o: o.levels + 1, "<u8", torch.uint64)
+    node_key = _Lazy("node_key", lambda o: o.total_nodes, "<u4", torch.uint32)
+    node_start = _Lazy("node_start", lambda o: o.total_nodes, "<u4", torch.uint32)
+    rank_block = _Lazy("rank_block", lambda o: o.levels * o.blocks_per_level, "<u2", torch.uint16)
+    rank_super = _Lazy("rank_super", lambda o: o.levels * o.supers_per_level, "<u8", torch.uint64)
 
     def __init__(self, handle, device):
         self._h = handle
@@ -198,13 +222,6 @@ class WaveletTree(_SelectOps):
         self.blocks_per_level = int(t.blocks_per_level)
         self.supers_per_level = int(t.supers_per_level)
         self.total_nodes = int(t.total_nodes)
-        L = self.levels
-        self.bits = _view(t.bits, L * self.words_per_level, "<u8", torch.uint64, device)
-        self.level_node_ptr = _view(t.level_node_ptr, L + 1, "<u8", torch.uint64, device)
-        self.node_key = _view(t.node_key, self.total_nodes, "<u4", torch.uint32, device)
-        self.node_start = _view(t.node_start, self.total_nodes, "<u4", torch.uint32, device)
-        self.rank_block = _view(t.rank_block, L * self.blocks_per_level, "<u2", torch.uint16, device)
-        self.rank_super = _view(t.rank_super, L * self.supers_per_level, "<u8", torch.uint64, device)
 
     @property
     def handle(self):
