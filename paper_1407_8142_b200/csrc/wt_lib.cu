@@ -469,7 +469,13 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     chk(cudaGetLastError());
     rec.end();
     // ---- A4: node table of this group's levels l0+k_lo .. l0+k_lo+nk-1 ----
-    if (gb.nk) {
+    if (gb.nk && g == 0) {
+      rec.begin("k_nodes_count", 0);
+      k_root_nodes<<<1, 32, 0, s>>>(gb.Cseg, gb.tau, gb.k_lo, gb.nk, L, ncount, t->level_node_ptr, t->node_key,
+                                    t->node_start, err);
+      chk(cudaGetLastError());
+      rec.end();
+    } else if (gb.nk) {
       const uint64_t rstride = gb.max_rows;
       const unsigned cgrid = (unsigned)std::min<uint64_t>((gb.max_rows * gb.nk * 32 + 255) / 256, 65535);
       rec.begin("k_nodes_count", 0);

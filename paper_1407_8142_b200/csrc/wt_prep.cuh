@@ -266,6 +266,44 @@ static __global__ void __launch_bounds__(1024) k_scan_rows_2(uint32_t *__restric
   if (threadIdx.x == 0) ncount[l0 + k_lo + blockIdx.x] = carry;
 }
 
+// Node table of group 0 (one row: the root, l0 = 0) in one warp: levels
+// k_lo .. k_lo+nk-1 in order, non-empty classes of the root's digit scan
+// Cseg[0] (Fig. 1 l.18-20); also ncount[] and level_node_ptr[] of those
+// levels.  Replaces the count / scan / emit passes of the general case.
+static __global__ void k_root_nodes(const uint32_t *__restrict__ Cseg, uint32_t tau, uint32_t k_lo, uint32_t nk,
+                                    uint32_t L, uint32_t *__restrict__ ncount, uint64_t *__restrict__ level_node_ptr,
+                                    uint32_t *__restrict__ node_key, uint32_t *__restrict__ node_start,
+                                    const uint32_t *err) {
+  if (*err || blockIdx.x || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const uint32_t lt = lanemask_lt();
+  uint64_t j = 0;
+  for (uint32_t kk = 0; kk < nk; kk++) {
+    const uint32_t k = k_lo + kk, sh = tau - k;
+    if (lane == 0) level_node_ptr[k] = j;
+    uint32_t c = 0;
+    for (uint32_t q0 = 0; q0 < (1u << k); q0 += 32) {
+      const uint32_t q = q0 + lane;
+      uint32_t a = 0, b = 0;
+      if (q < (1u << k)) {
+        a = Cseg[q << sh];
+        b = Cseg[(q + 1) << sh];
+      }
+      const uint32_t bm = __ballot_sync(FULL, b > a);
+      if (b > a) {
+        node_key[j + __popc(bm & lt)] = q;
+        node_start[j + __popc(bm & lt)] = a;
+      }
+      j += __popc(bm);
+      c += __popc(bm);
+    }
+    if (lane == 0) {
+      ncount[k] = c;
+      if (k + 1 == L) level_node_ptr[L] = j;
+    }
+  }
+}
+
 // Level CSR bases: level_node_ptr[lev] for the group's levels (runs after pass 2).
 static __global__ void k_level_ptr(const uint32_t *__restrict__ ncount, uint32_t l0, uint32_t k_lo, uint32_t nk, uint32_t L,
                             uint64_t *__restrict__ level_node_ptr, const uint32_t *err) {
