@@ -252,16 +252,15 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            tree = wt.build(S_dev, cfg.sigma, stream)
-            prof = wt.last_profile()
-            tree.free()
-            launches += prof["total_launches"]
-            for k in prof["kernels"]:
-                kern_ms[k["name"]] = kern_ms.get(k["name"], 0.0) + k["ms"]
-                kern_bytes[k["name"]] = kern_bytes.get(k["name"], 0) + k["algo_bytes"]
-                kern_launch[k["name"]] = kern_launch.get(k["name"], 0) + k["launches"]
+            wt.build(S_dev, cfg.sigma, stream).free()
         e1.record(stream)
         torch.cuda.synchronize()
+    prof = wt.last_profile(total=True)  # per-kernel events of the K timed builds, summed
+    launches = prof["total_launches"]
+    for k in prof["kernels"]:
+        kern_ms[k["name"]] = k["ms"]
+        kern_bytes[k["name"]] = k["algo_bytes"]
+        kern_launch[k["name"]] = k["launches"]
     barrier()
     wt.profile_enable(False)
     ms_local = e0.elapsed_time(e1) / args.steps

@@ -105,8 +105,9 @@ int wt_build(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma,
 int wt_build_host(const void *h_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma,
                   void *stream, wt_tree **out);
 
-/* wt_free -- release everything owned by t (synchronises the device as
- * needed).  NULL is a no-op.  Returns WT_OK or WT_ECUDA. */
+/* wt_free -- release everything owned by t: stream-ordered frees on the
+ * build's stream (after any work queued there, e.g. queries).  NULL is a
+ * no-op.  Returns WT_OK or WT_ECUDA. */
 int wt_free(wt_tree *t);
 
 /*
@@ -329,11 +330,15 @@ typedef struct wt_profile {
   wt_prof_entry e[WT_PROF_MAX];
 } wt_profile;
 
-/* Enable (1) / disable (0) per-kernel event timing in subsequent builds. */
+/* Enable (1) / disable (0) per-kernel event timing in subsequent builds;
+ * enabling also resets the total of wt_profile_total. */
 int wt_profile_enable(int on);
 /* Copy the per-kernel record of the most recent build (profiled or not:
  * launches and total_launches are always filled, ms only when enabled). */
 int wt_last_profile(wt_profile *out);
+/* The per-kernel record summed over every build since profiling was last
+ * enabled (bench.py reads it once after the timed steps). */
+int wt_profile_total(wt_profile *out);
 /* Version string of the library. */
 const char *wt_version(void);
 

@@ -23,7 +23,7 @@ namespace wthost {
 
 struct Prof {
   bool enabled = false;
-  wt_profile last{};
+  wt_profile last{}, total{};  // the last build; all builds since profiling was enabled
   std::mutex mu;
 };
 inline Prof g_prof;
@@ -35,6 +35,27 @@ struct Launch {
 };
 
 // Per-build recorder of kernel launches (optionally timed with events).
+// timing events are recycled per host thread (creating events per build
+// would add host latency between the builds being timed)
+inline std::vector<cudaEvent_t> &event_pool() {
+  static thread_local std::vector<cudaEvent_t> pool;
+  return pool;
+}
+inline cudaEvent_t event_get() {
+  auto &pool = event_pool();
+  if (pool.empty()) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = pool.back();
+  pool.pop_back();
+  return e;
+}
+inline void event_put(cudaEvent_t e) {
+  if (e) event_pool().push_back(e);
+}
+
 struct Recorder {
   cudaStream_t s;
   bool timed;
@@ -47,8 +68,8 @@ struct Recorder {
     L.algo_bytes = bytes;
     cur = on ? on : s;
     if (timed) {
-      cudaEventCreate(&L.e0);
-      cudaEventCreate(&L.e1);
+      L.e0 = event_get();
+      L.e1 = event_get();
       cudaEventRecord(L.e0, cur);
     }
     launches.push_back(L);
@@ -63,8 +84,8 @@ struct Recorder {
       float ms = 0.f;
       if (timed) {
         cudaEventElapsedTime(&ms, L.e0, L.e1);
-        cudaEventDestroy(L.e0);
-        cudaEventDestroy(L.e1);
+        event_put(L.e0);
+        event_put(L.e1);
       }
       int k = -1;
       for (uint32_t i = 0; i < p.count; i++)
@@ -81,12 +102,28 @@ struct Recorder {
     }
     std::lock_guard<std::mutex> g(g_prof.mu);
     g_prof.last = p;
+    wt_profile &T = g_prof.total;  // accumulate by kernel name
+    T.total_launches += p.total_launches;
+    for (uint32_t i = 0; i < p.count; i++) {
+      int k = -1;
+      for (uint32_t j = 0; j < T.count; j++)
+        if (!strcmp(T.e[j].name, p.e[i].name)) k = (int)j;
+      if (k < 0 && T.count < WT_PROF_MAX) {
+        k = (int)T.count++;
+        memcpy(T.e[k].name, p.e[i].name, sizeof(T.e[k].name));
+      }
+      if (k >= 0) {
+        T.e[k].ms += p.e[i].ms;
+        T.e[k].launches += p.e[i].launches;
+        T.e[k].algo_bytes += p.e[i].algo_bytes;
+      }
+    }
   }
   void discard() {
     if (timed)
       for (auto &L : launches) {
-        cudaEventDestroy(L.e0);
-        cudaEventDestroy(L.e1);
+        event_put(L.e0);
+        event_put(L.e1);
       }
   }
 };

@@ -594,12 +594,10 @@ int wt_free(wt_tree *t) {
   Internal *in = static_cast<Internal *>(t->internal);
   cudaError_t e = cudaSuccess;
   if (in) {
-    for (void *p : in->outputs) {
+    for (void *p : in->outputs) {  // stream-ordered: after the work queued on the build stream
       cudaError_t e2 = cudaFreeAsync(p, in->stream);
       if (e2 != cudaSuccess) e = e2;
     }
-    cudaError_t e3 = cudaStreamSynchronize(in->stream);
-    if (e3 != cudaSuccess) e = e3;
     delete in;
   }
   delete t;
@@ -639,6 +637,14 @@ int wt_rank(const wt_tree *t, const uint32_t *d_sym, const uint64_t *d_pos, uint
 int wt_profile_enable(int on) {
   std::lock_guard<std::mutex> g(g_prof.mu);
   g_prof.enabled = on != 0;
+  if (on) g_prof.total = wt_profile{};
+  return WT_OK;
+}
+
+int wt_profile_total(wt_profile *out) {
+  if (!out) return WT_EINVAL;
+  std::lock_guard<std::mutex> g(g_prof.mu);
+  *out = g_prof.total;
   return WT_OK;
 }
 

@@ -105,6 +105,8 @@ def _load():
     lib.wt_profile_enable.restype = ctypes.c_int
     lib.wt_last_profile.argtypes = [ctypes.POINTER(_Profile)]
     lib.wt_last_profile.restype = ctypes.c_int
+    lib.wt_profile_total.argtypes = [ctypes.POINTER(_Profile)]
+    lib.wt_profile_total.restype = ctypes.c_int
     lib.wt_version.argtypes = []
     lib.wt_version.restype = ctypes.c_char_p
     PM = ctypes.POINTER(_WmMatrix)
@@ -344,9 +346,11 @@ def profile_enable(on: bool = True) -> None:
     _load().wt_profile_enable(1 if on else 0)
 
 
-def last_profile() -> dict:
+def last_profile(total: bool = False) -> dict:
+    """Per-kernel record of the last build (or, with total=True, summed over
+    every build since profile_enable(True))."""
     p = _Profile()
-    _load().wt_last_profile(ctypes.byref(p))
+    (_load().wt_profile_total if total else _load().wt_last_profile)(ctypes.byref(p))
     ents = []
     for i in range(p.count):
         e = p.e[i]
