@@ -83,10 +83,9 @@ int wm_build_impl(const void *d_seq, uint64_t n, uint32_t eb, uint64_t sigma, vo
   m->words_per_level = WPL;
   m->blocks_per_level = BPL;
   m->supers_per_level = SPL;
-  m->bits = A.alloc<uint64_t>(L * WPL, true);
-  m->zeros = A.alloc<uint64_t>(L, true);
-  m->rank_block = A.alloc<uint16_t>(L * BPL, true);
-  m->rank_super = A.alloc<uint64_t>(L * SPL, true);
+  A.use_arena();
+  A.alloc_outputs({{(void **)&m->bits, L * WPL * 8}, {(void **)&m->zeros, L * 8}, {(void **)&m->rank_block, L * BPL * 2},
+                   {(void **)&m->rank_super, L * SPL * 8}});
   uint32_t *err = A.alloc<uint32_t>(4, false);
   uint64_t *suptot = A.alloc<uint64_t>(L * NSD, false);
   const uint32_t NG = (L + TAU_MAX - 1) / TAU_MAX;
