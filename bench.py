@@ -52,12 +52,12 @@ def peaks():
 
 class ClockSampler:
     """SM clock and throttle-reason sampling during the timed region (NVML,
-    every 20 ms; the nvidia-smi query of B200_PROFILING.md as a fallback)."""
+    every 5 ms plus one at the end; the nvidia-smi query of B200_PROFILING.md as a fallback)."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
 
-    def __init__(self, gpu_index: int, period_s: float = 0.02):
+    def __init__(self, gpu_index: int, period_s: float = 0.005):
         self.idx = gpu_index
         self.period = period_s
         self.sm, self.mx, self.reasons = [], [], set()
@@ -111,6 +111,10 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        try:  # one more sample at the end of the timed region (short regions)
+            self._sample_nvml() if self._nvml else self._sample_smi()
+        except Exception:
+            pass
 
     def summary(self):
         if not self.sm:
