@@ -1,5 +1,6 @@
 """Per-config build report (SURVEY §8(d) "Report, per config"): device time of
-wt_build (median of 5 after 2 warm-ups, CUDA events), elements/s,
+wt_build (median of 5 after 2 warm-ups, CUDA events, a 512 MB write before
+each timed build so that no input or output is L2-resident), elements/s,
 symbol-levels/s, B_min / t.  JSON lines to stdout and gpurun_out/report_time.jsonl.
 DRAM bytes and instructions come from the ncu pass in tools/gpu_report.sh."""
 import json, os, statistics, sys
@@ -16,13 +17,15 @@ def bmin(n, w, L):
     return n * w + L * bpl * 8 * 8 + L * (2 * bpl + 8 * ((n + 65535) // 65536 + 1))
 
 
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2: evicted before each timed build
 for ci in [int(x) for x in sys.argv[1:]] or [1, 2, 3, 4, 5]:
     cfg = gen.CONFIGS[ci]
     S = torch.from_numpy(gen.config_input(cfg)).cuda()
     for _ in range(2):
         wt.build(S, cfg.sigma).free()
     ts, nodes = [], 0
-    for _ in range(5):
+    for i in range(5):
+        flush.fill_(i)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(); t = wt.build(S, cfg.sigma); e1.record(); torch.cuda.synchronize()
