@@ -185,3 +185,13 @@ def test_hwt_select_vs_oracle(sigma, n):
     got = t.select(torch.from_numpy(cs.view(np.int32)).cuda(), torch.from_numpy(ks).cuda()).cpu().numpy()
     assert np.array_equal(got, want)
     t.free()
+
+
+@pytest.mark.slow
+def test_hwt_full_config4():
+    """Config 4 (n = 2^28 u32, sigma = 2^16: 16-bit codes, one stage) at full size."""
+    cfg = gen.CONFIGS[4]
+    S = gen.config_input(cfg)
+    t = _compare(S, cfg.sigma)
+    _queries(t, S, cfg.sigma, k=1000, seed=4)
+    t.free()
