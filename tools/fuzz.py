@@ -1,5 +1,6 @@
 """Randomised parity fuzzing of every structure against the oracle (not part of
-the test suite; run on the GPU box for a time budget).  usage: fuzz.py SECONDS [seed]"""
+the test suite; run on the GPU box for a time budget).
+usage: fuzz.py SECONDS [seed] [max_n]"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -8,12 +9,13 @@ import paper_1407_8142_b200 as wt
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 60
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+MAXN = int(sys.argv[3]) if len(sys.argv) > 3 else 400000
 t_end = time.time() + budget
 cases = fails = 0
 
 
 def gen_seq():
-    n = int(np.exp(rng.uniform(0, np.log(400000))))
+    n = int(np.exp(rng.uniform(0, np.log(MAXN))))
     if rng.random() < 0.1:
         n = int(rng.integers(0, 70))
     sigma = int(np.exp(rng.uniform(0, np.log(2.0 ** 32))))
