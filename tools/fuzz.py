@@ -65,10 +65,28 @@ while time.time() < t_end:
         t = wt.build(St, sigma)
         ok = check("wt " + tag, t.numpy(), oracle.build(S, sigma),
                    ("bits", "level_node_ptr", "node_key", "node_start", "rank_block", "rank_super"))
-        if ok and S.size and t.levels:
+        if ok and S.size:
             pos = rng.integers(0, S.size, 200)
             if not np.array_equal(t.access(torch.from_numpy(pos).cuda()).cpu().numpy(), S[pos].astype(np.uint32)):
                 print("FAIL access", tag, flush=True); fails += 1
+            if S.size <= 200000:  # rank / select against brute force (stable sort of S)
+                order = np.argsort(S, kind="stable")
+                Ss = S[order]
+                cs = S[rng.integers(0, S.size, 100)].astype(np.uint64)
+                lo = np.searchsorted(Ss, cs)
+                cnt = np.searchsorted(Ss, cs, side="right") - lo
+                rank_want = np.array([np.count_nonzero(order[a:a + c] <= p) for a, c, p in zip(lo, cnt, pos[:100])],
+                                     dtype=np.uint64)
+                c32 = torch.from_numpy(cs.astype(np.uint32).view(np.int32)).cuda()
+                p64 = torch.from_numpy(pos[:100].astype(np.int64)).cuda()
+                ks = np.maximum(1, (rng.random(100) * cnt).astype(np.int64) + 1)
+                k64 = torch.from_numpy(ks).cuda()
+                sel_want = order[lo + ks - 1].astype(np.uint64)
+                for nm, obj in (("wt", t),):
+                    if not np.array_equal(obj.rank(c32, p64).cpu().numpy(), rank_want):
+                        print("FAIL rank", nm, tag, flush=True); fails += 1
+                    if not np.array_equal(obj.select(c32, k64).cpu().numpy(), sel_want):
+                        print("FAIL select", nm, tag, flush=True); fails += 1
         t.free()
         m = wt.wm_build(St, sigma)
         check("wm " + tag, m.numpy(), oracle.wm_build(S, sigma), ("bits", "zeros", "rank_block", "rank_super"))
