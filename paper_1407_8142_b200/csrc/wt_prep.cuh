@@ -92,6 +92,11 @@ static __global__ void __launch_bounds__(1024) k_chains_from_nodes(
 // A1 / per-chain digit histogram: one CTA per chain; 16-byte streaming loads;
 // for the root pass also validates S[i] < sigma.
 // histT[d][c] = count of digit d in chain c (transposed for the scans).
+// Shared counters are lane-major, h[d * 32 + lane]: every lane of a warp owns
+// its own bank, so the per-element atomics are free of bank conflicts (with
+// bins shared by the lanes the random digits of a warp collide in ~3.5-way
+// bank conflicts and the atomics replay).  The reduction reads column
+// (j + d) mod 32 so that consecutive digits hit distinct banks.
 // ---------------------------------------------------------------------------
 template <typename T, bool VALIDATE>
 __global__ void __launch_bounds__(512) k_chain_hist(const T *__restrict__ keys, uint64_t sigma, uint32_t shift,
@@ -99,21 +104,22 @@ __global__ void __launch_bounds__(512) k_chain_hist(const T *__restrict__ keys, 
                                                    const uint32_t *__restrict__ chain_end,
                                                    const uint32_t *__restrict__ counts, uint32_t stride,
                                                    uint32_t *__restrict__ histT, uint32_t *err) {
-  __shared__ uint32_t h[NDIG * 4];  // 4 sub-histograms spread same-bin contention
+  __shared__ uint32_t h[NDIG * 32];
   if (!VALIDATE && ld_relaxed(err)) return;
   const uint32_t nchains = counts[0];
+  const uint32_t lane = threadIdx.x & 31;
   bool bad = false;
   for (uint32_t c = blockIdx.x; c < nchains; c += gridDim.x) {
-  for (uint32_t i = threadIdx.x; i < 4 * NDIG; i += blockDim.x) h[i] = 0;
+  for (uint32_t i = threadIdx.x; i < 32 * ndig; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  uint32_t *hs = h + (threadIdx.x & 3) * NDIG;
+  uint32_t *hs = h + lane;
   const uint32_t dmask = ndig - 1u;
   auto add = [&](uint32_t v) {
     if (VALIDATE && (uint64_t)v >= sigma) {
       bad = true;
       return;
     }
-    atomicAdd(&hs[(v >> shift) & dmask], 1u);
+    atomicAdd(&hs[((v >> shift) & dmask) << 5], 1u);
   };
   const uint32_t beg = chain_begin[c], end = chain_end[c];
   constexpr int PER = 16 / sizeof(T);
@@ -133,8 +139,12 @@ __global__ void __launch_bounds__(512) k_chain_hist(const T *__restrict__ keys, 
     }
   }
   __syncthreads();
-  for (uint32_t d = threadIdx.x; d < ndig; d += blockDim.x)
-    histT[(uint64_t)d * stride + c] = h[d] + h[NDIG + d] + h[2 * NDIG + d] + h[3 * NDIG + d];
+  for (uint32_t d = threadIdx.x; d < ndig; d += blockDim.x) {
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (uint32_t j = 0; j < 32; j++) sum += h[(d << 5) + ((j + d) & 31u)];
+    histT[(uint64_t)d * stride + c] = sum;
+  }
   __syncthreads();
   }
   if (VALIDATE && __any_sync(FULL, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
