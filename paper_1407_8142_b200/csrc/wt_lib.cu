@@ -8,6 +8,7 @@
 // and the node counts.
 #include "wt_host.cuh"
 #include "wt_group.cuh"
+#include "wt_wgroup.cuh"
 #include "wt_local.cuh"
 #include "wt_prep.cuh"
 #include "wt_rank.cuh"
@@ -25,6 +26,8 @@ struct GroupLaunch {
   void (*kern)(GroupParams) = nullptr;
   size_t smem = 0;
   int grid = 0;
+  int threads = 0;
+  int workers = 0;    // independent chain workers (CTAs, or warps for k_wgroup)
   uint32_t tile = 0;  // positions per tile (chains are cut at multiples of it)
 };
 
@@ -36,11 +39,42 @@ GroupLaunch group_launch() {
     gl.kern = k_group<InT, RecT, OutT, HAS_OUT>;
     gl.smem = 0;  // static shared memory
     gl.tile = GroupTile<RecT>::TT;
+    gl.threads = WPB * 32;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl.kern, WPB * 32, 0);
     gl.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
+    gl.workers = gl.grid;
   });
   return gl;
+}
+
+// k_wgroup: one chain per CTA at a time, dynamic shared memory
+template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
+GroupLaunch wgroup_launch() {
+  static GroupLaunch gl;
+  static std::once_flag f;
+  std::call_once(f, [] {
+    gl.kern = k_wgroup<InT, RecT, OutT, HAS_OUT>;
+    gl.smem = sizeof(WGSmem<InT, RecT, HAS_OUT>);
+    gl.tile = WGTile<RecT>::T;
+    gl.threads = CT_WARPS * 32;
+    cudaFuncSetAttribute(gl.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gl.smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl.kern, gl.threads, gl.smem);
+    gl.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
+    gl.workers = gl.grid;  // one chain per CTA at a time
+  });
+  return gl;
+}
+
+inline bool use_old_group() {
+  static const bool old = getenv("WT_OLD_GROUP") != nullptr;
+  return old;
+}
+
+template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
+GroupLaunch any_group_launch() {
+  return use_old_group() ? group_launch<InT, RecT, OutT, HAS_OUT>() : wgroup_launch<InT, RecT, OutT, HAS_OUT>();
 }
 
 struct LocalLaunch {
@@ -97,19 +131,19 @@ LocalLaunch pick_local(uint32_t inw, uint32_t recw, uint32_t outw, bool has_out)
 GroupLaunch pick_group_mode(uint32_t inw, uint32_t recw, uint32_t outw, bool has_out) {
   if (!has_out) {
     if (recw == 1) {
-      if (inw == 1) return group_launch<uint8_t, uint8_t, uint8_t, false>();
-      if (inw == 2) return group_launch<uint16_t, uint8_t, uint8_t, false>();
-      return group_launch<uint32_t, uint8_t, uint8_t, false>();
+      if (inw == 1) return any_group_launch<uint8_t, uint8_t, uint8_t, false>();
+      if (inw == 2) return any_group_launch<uint16_t, uint8_t, uint8_t, false>();
+      return any_group_launch<uint32_t, uint8_t, uint8_t, false>();
     }
     return GroupLaunch{};  // the last group always has <= 8 bits per record
   }
   if (recw == 2) {
-    if (inw == 2) return group_launch<uint16_t, uint16_t, uint8_t, true>();
-    return group_launch<uint32_t, uint16_t, uint8_t, true>();
+    if (inw == 2) return any_group_launch<uint16_t, uint16_t, uint8_t, true>();
+    return any_group_launch<uint32_t, uint16_t, uint8_t, true>();
   }
   // recw == 4
-  if (outw == 2) return group_launch<uint32_t, uint32_t, uint16_t, true>();
-  return group_launch<uint32_t, uint32_t, uint32_t, true>();
+  if (outw == 2) return any_group_launch<uint32_t, uint32_t, uint16_t, true>();
+  return any_group_launch<uint32_t, uint32_t, uint32_t, true>();
 }
 
 // Per-group scratch: chains, rows, digit tables, node-count scans.
@@ -247,9 +281,9 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       gb.ndefer = n / (LT + 1) + 1;
       gb.max_chains = 1;
     } else {
-      const uint64_t warps = (uint64_t)gb.gl.grid;  // CTAs (one chain at a time each)
-      static const uint64_t cpw =
-          getenv("WT_CHAINS_PER_WARP") ? strtoull(getenv("WT_CHAINS_PER_WARP"), 0, 10) : 16;
+      const uint64_t warps = (uint64_t)gb.gl.workers;  // chain workers (one chain at a time each)
+      static const uint64_t cpw = getenv("WT_CHAINS_PER_WARP") ? strtoull(getenv("WT_CHAINS_PER_WARP"), 0, 10)
+                                                              : 16;
       const uint64_t target = (n + cpw * warps - 1) / (cpw * warps);
       const uint64_t tt = gb.gl.tile;
       gb.CH = std::max<uint64_t>(tt, ((target + tt - 1) / tt) * tt);
@@ -520,7 +554,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     char name[32];
     snprintf(name, sizeof(name), "k_group%u", g);
     rec.begin(name, n * gb.inw + (has_out ? n * gb.outw : 0) + (uint64_t)gb.tau * n / 8);
-    gb.gl.kern<<<gb.gl.grid, WPB * 32, 0, s>>>(gp);
+    gb.gl.kern<<<gb.gl.grid, gb.gl.threads, gb.gl.smem, s>>>(gp);
     chk(cudaGetLastError());
     rec.end();
     rank_levels(gb.l0, gb.tau);

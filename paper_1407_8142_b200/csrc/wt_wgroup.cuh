@@ -1,0 +1,670 @@
+// wt_wgroup.cuh -- the hot kernel, round 2: one HBM pass builds tau <= 8
+// consecutive levels l0 .. l0+tau-1 of the levelwise wavelet tree (SURVEY
+// §8(a) A2, A3, A5, A6), one independent WARP per chain.
+//
+// What a warp computes (Fig. 1 l.12-17, restated for a tile): a chain
+// is <= CH consecutive positions of S_{l0} inside one level-l0 node (its
+// "row"); it is processed in sub-tiles of <= T positions held in the warp's
+// own shared memory.  Inside a sub-tile the warp keeps the records in the
+// sub-tile's *wavelet-matrix order* M_k (the sub-tile stably sorted by the
+// reversed top-k digit bits): going from M_k to M_{k+1} is ONE
+// stable zeros-first split of the whole sub-tile by bit k, so no per-node
+// (per-class) split tables are needed.  A class of level k (the elements of
+// one level-(l0+k) node) is a contiguous run of M_k in
+// original order -- the same run it forms in S_{l0+k} --
+// so level l0+k's bitmap is M_k's bitmap with the class runs placed at their
+// tree positions.
+//
+// Records: rec = bit-reverse of the key over its kb = L - l0 remaining bits,
+// so the level-(l0+k) bit (the (l+1)'st highest bit) is rec bit
+// k and the reversed digit rd = rec & (2^tau - 1) is the class index r of
+// level tau in M_tau order.
+//
+// The split (per level, per 32*E-position "superchunk", E = 8 / sizeof(rec)):
+// lane l holds E consecutive records (one 8-byte LDS); the level bits t_j,
+// their exclusive in-lane prefix (SWAR: one IMAD per 4 bytes), the lane's
+// count and the cross-lane exclusive prefix O (ballots of the count's bits +
+// POPC) give every element its rank in its own stream; the destination is
+//     bit 0: dst + zeros_before(superchunk) + (E*lane - O) + (j - pre_j)
+//     bit 1: dst + Z + ones_before(superchunk) + O + pre_j
+// (Fig. 1 l.15-17: zeros to start + X[i], ones to start + X_s + i - X[i]),
+// evaluated for two elements at a time with one dp2a each.  The level's
+// bitmap bytes and the ones-before count of every byte (a byte-grain rank
+// directory of the sub-tile) are written to shared memory; class counts of
+// level k+1 follow from rank queries at the class boundaries of level k, so
+// no per-tile digit histogram is built.  Padding records (all ones) fill the
+// last superchunk: they are ones at every level and stay at the end.
+//
+// Global placement (A5): class r of level k goes to the
+// running position pos[slot], slot = 2^k + r, initialised per chain from the
+// chain tables (E, Cseg of wt_prep.cuh); words inside a run are stored, the
+// partial last word of a run is carried to the next sub-tile of the chain,
+// words shared with another chain or node are OR-ed atomically into the
+// zero-initialised bitmap.
+#pragma once
+#include "wt_common.cuh"
+#include "wt_group.cuh"  // GroupParams, CF_VALID / CF_SHARED
+
+namespace wtb {
+
+#ifndef WT_CT_WARPS
+#define WT_CT_WARPS 4
+#endif
+constexpr int CT_WARPS = WT_CT_WARPS;  // warps of a CTA; they share one tile, each splits a quarter
+#ifndef WT_WG_UNROLL
+#define WT_WG_UNROLL 2
+#endif
+constexpr int WG_UNROLL = WT_WG_UNROLL;  // superchunks of the split loop unrolled
+
+template <typename RecT>
+struct WGTile {
+  static constexpr int E = sizeof(RecT) == 4 ? 2 : 8;  // records per lane per superchunk (one LDS)
+  static constexpr int SC = 32 * E;                      // positions per superchunk
+#ifndef WT_CT_TB
+#define WT_CT_TB 8192
+#endif
+  static constexpr int T = WT_CT_TB / (int)sizeof(RecT);  // records per tile (WT_CT_TB bytes of records)
+  static constexpr int SPW = T / SC / CT_WARPS;           // superchunks per warp
+  static_assert(SPW >= 1 && T % (SC * CT_WARPS) == 0, "whole superchunks per warp");
+};
+
+template <typename InT, typename RecT, bool HAS_OUT>
+struct WGSmem {
+  static constexpr int T = WGTile<RecT>::T;
+  static constexpr int LBB = T / 8 + 16;  // bytes per level bitmap (+ slack for 3-word reads)
+  static constexpr int RPW = T / 32 + 2;  // word ranks per level (+ the padded end)
+  alignas(16) RecT rec[2][T];
+  alignas(16) uint8_t stage[T * sizeof(InT) + 32];  // raw input of the next tile (TMA bulk copy)
+  alignas(16) uint8_t LB[TAU_MAX][LBB];  // level bitmaps of the tile (M_k order)
+  alignas(16) uint16_t RP[TAU_MAX][RPW]; // ones of the level before each 32-bit word of LB
+  alignas(16) uint32_t pos[256];         // running global bit position of slot 2^k + r
+  alignas(16) uint32_t kpos[HAS_OUT ? 256 : 1];  // running key position per (true) digit
+  alignas(16) unsigned long long CW[256];        // carried partial word per slot (chain setup: scratch)
+  alignas(16) uint16_t C[512];           // class counts (real) of slot 2^k + r, k <= tau
+  alignas(16) uint16_t S[512];           // class starts (tile positions in M_k)
+  alignas(16) uint32_t Zs[TAU_MAX + 2];  // zeros of each level's bit (real elements)
+  alignas(16) uint32_t onesW[CT_WARPS];  // ones of the current bit in each warp's quarter
+  alignas(16) unsigned long long bar;    // mbarrier of the bulk copy
+  uint32_t chain, cnext;
+  alignas(16) uint8_t CF[256];           // carry flags per slot
+};
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+// ballot of (v & m) != 0
+__device__ __forceinline__ uint32_t ballot_m(uint32_t v, uint32_t m) {
+  uint32_t r;
+  asm(
+      "{.reg .pred p; .reg .b32 t; and.b32 t, %1, %2; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 %0, p, 0xffffffff;}"
+      : "=r"(r)
+      : "r"(v), "r"(m));
+  return r;
+}
+__device__ __forceinline__ uint32_t rev_bits(uint32_t x, uint32_t nb) { return nb ? __brev(x) >> (32u - nb) : 0u; }
+
+// ---------------------------------------------------------------------------
+// One level of one sub-tile: the level's bitmap (LB, M_k order) and the ones
+// before every 32-bit word of it (RP), optionally the stable split src -> dst
+// (byte addresses), and the ones of bit k+1 (returned, padding included).
+// nsc superchunks; Z = zeros of bit k.
+// ---------------------------------------------------------------------------
+template <typename RecT, bool MOVE>
+__device__ __forceinline__ void wg_split(uint8_t *LB, uint16_t *RP, uint32_t src, uint32_t dst, uint32_t c0,
+                                         uint32_t c1, uint32_t nsc, uint32_t k, uint32_t Z, uint32_t SP0, int lane,
+                                         uint32_t lt) {
+  constexpr uint32_t E = WGTile<RecT>::E, SC = WGTile<RecT>::SC, RB = sizeof(RecT);
+  constexpr uint32_t LANEB = E * RB;                // record bytes per lane per superchunk
+  const uint32_t lbA = smem_u32(LB), rpA = smem_u32(RP);
+  const uint32_t sA = src + lane * LANEB;
+  uint32_t SP = SP0;                                // ones before the superchunk (level k)
+  uint32_t Bo = dst + (Z + SP0) * RB;               // ones region + ones so far
+  uint32_t Bz = dst + (c0 * SC - SP0) * RB + lane * LANEB;  // zeros so far + this lane's first slot
+  if constexpr (RB == 1) {
+    // software pipelined: the next superchunk's load is issued before this one is processed
+    uint2 xn = lds64(sA + c0 * (SC * RB));
+#pragma unroll(WG_UNROLL)
+    for (uint32_t c = c0; c < c1; c++) {
+      const uint2 x = xn;
+      if (c + 1 < c1) xn = lds64(sA + (c + 1) * (SC * RB));
+      const uint32_t t_lo = (x.x >> k) & 0x01010101u, t_hi = (x.y >> k) & 0x01010101u;
+      const uint32_t pre_lo = t_lo * 0x01010100u;
+      const uint32_t inc_lo = pre_lo + t_lo;
+      const uint32_t pre_hi = t_hi * 0x01010100u + __byte_perm(inc_lo, 0, 0x3333);
+      const uint32_t inc = pre_hi + t_hi;  // byte 3: ones of the lane (0..8)
+      const uint32_t O = __popc(ballot_m(inc, 1u << 24) & lt) + 2 * __popc(ballot_m(inc, 2u << 24) & lt) +
+                         4 * __popc(ballot_m(inc, 4u << 24) & lt) + 8 * __popc(ballot_m(inc, 8u << 24) & lt);
+      const uint32_t Sc = __shfl_sync(FULL, O + (inc >> 24), 31);
+      if (!(lane & 3)) sts16(rpA + (c * 8u + (lane >> 2)) * 2u, SP + O);
+      // bits 24..27 <- elements 0..3, bits 28..31 <- elements 4..7 (disjoint products, no carries)
+      sts8(lbA + c * 32u + lane, (t_lo * 0x01020408u + t_hi * 0x10204080u) >> 24);
+      if constexpr (MOVE) {
+        const uint32_t D0 = Bz - O;
+        const uint32_t A = (Bo + O - D0) | 0x10000u;
+        const uint32_t M_lo = t_lo * 0xffu, M_hi = t_hi * 0xffu;
+        const uint32_t q_lo = (pre_lo & M_lo) | ((0x03020100u - pre_lo) & ~M_lo);
+        const uint32_t q_hi = (pre_hi & M_hi) | ((0x07060504u - pre_hi) & ~M_hi);
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+          const uint32_t q = w ? q_hi : q_lo, t = w ? t_hi : t_lo, r = w ? x.y : x.x;
+          const uint32_t tq0 = __byte_perm(t, q, 0x5140), tq1 = __byte_perm(t, q, 0x7362);
+          sts8(__dp2a_lo(A, tq0, D0), r);
+          sts8(__dp2a_hi(A, tq0, D0), __byte_perm(r, 0, 0x1));
+          sts8(__dp2a_lo(A, tq1, D0), __byte_perm(r, 0, 0x2));
+          sts8(__dp2a_hi(A, tq1, D0), __byte_perm(r, 0, 0x3));
+        }
+      }
+      SP += Sc;
+      Bo += Sc;
+      Bz += SC - Sc;
+    }
+  } else if constexpr (RB == 2) {
+    uint4 xn = lds128(sA + c0 * (SC * RB));
+#pragma unroll(WG_UNROLL)
+    for (uint32_t c = c0; c < c1; c++) {
+      const uint32_t x[4] = {xn.x, xn.y, xn.z, xn.w};
+      if (c + 1 < c1) xn = lds128(sA + (c + 1) * (SC * RB));
+      uint32_t t[4], pre[4];
+#pragma unroll
+      for (int w = 0; w < 4; w++) t[w] = (x[w] >> k) & 0x00010001u;
+      uint32_t cin = 0, inc = 0;
+#pragma unroll
+      for (int w = 0; w < 4; w++) {  // exclusive prefix in 16-bit fields
+        pre[w] = (t[w] << 16) + cin;
+        inc = pre[w] + t[w];
+        cin = __byte_perm(inc, 0, 0x3232);
+      }
+      // high half of inc: ones of the lane (0..8)
+      const uint32_t O = __popc(ballot_m(inc, 1u << 16) & lt) + 2 * __popc(ballot_m(inc, 2u << 16) & lt) +
+                         4 * __popc(ballot_m(inc, 4u << 16) & lt) + 8 * __popc(ballot_m(inc, 8u << 16) & lt);
+      const uint32_t Sc = __shfl_sync(FULL, O + (inc >> 16), 31);
+      if (!(lane & 3)) sts16(rpA + (c * 8u + (lane >> 2)) * 2u, SP + O);
+      const uint32_t u = t[0] | (t[1] << 2) | (t[2] << 4) | (t[3] << 6);
+      sts8(lbA + c * 32u + lane, u | (u >> 15));  // element j of the lane -> bit j
+      if constexpr (MOVE) {
+        const uint32_t D0 = Bz - 2u * O;
+        const uint32_t A = (Bo + 2u * O - D0) | 0x20000u;
+#pragma unroll
+        for (int w = 0; w < 4; w++) {
+          const uint32_t M = t[w] * 0xffffu;
+          const uint32_t q = (pre[w] & M) | ((0x00010000u + 0x00020002u * w - pre[w]) & ~M);
+          const uint32_t tq = __byte_perm(t[w], q, 0x6240);
+          sts16(__dp2a_lo(A, tq, D0), x[w]);
+          sts16(__dp2a_hi(A, tq, D0), x[w] >> 16);
+        }
+      }
+      SP += Sc;
+      Bo += 2u * Sc;
+      Bz += 2u * (SC - Sc);
+    }
+  } else {
+#pragma unroll 2
+    for (uint32_t c = c0; c < c1; c++) {
+      const uint2 x = lds64(sA + c * (SC * RB));
+      const uint32_t t0 = (x.x >> k) & 1u, t1 = (x.y >> k) & 1u;
+      const uint32_t tot = t0 + t1;
+      const uint32_t O = __popc(ballot_m(tot, 1u) & lt) + 2 * __popc(ballot_m(tot, 2u) & lt);
+      const uint32_t Sc = __shfl_sync(FULL, O + tot, 31);
+      uint32_t v = t0 | (t1 << 1);
+      v |= __shfl_down_sync(FULL, v, 1) << 2;
+      v |= __shfl_down_sync(FULL, v, 2) << 4;
+      if (!(lane & 15)) sts16(rpA + (c * 2u + (lane >> 4)) * 2u, SP + O);
+      if (!(lane & 3)) sts8(lbA + c * 8u + (lane >> 2), v);
+      if constexpr (MOVE) {
+        const uint32_t D0 = Bz - 4u * O, D1 = Bo + 4u * O;
+        sts<uint32_t>(t0 ? D1 : D0, x.x);
+        sts<uint32_t>(t1 ? D1 + 4u * t0 : D0 + 4u * (1u - t0), x.y);
+      }
+      SP += Sc;
+      Bo += 4u * Sc;
+      Bz += 4u * (SC - Sc);
+    }
+  }
+  if (lane == 0 && c1 == nsc && c0 < c1) RP[nsc * SC / 32] = (uint16_t)SP;  // rank at the padded end
+}
+
+// ones of bit k over superchunks [c0, c1) of the tile (padding included), warp-reduced
+template <typename RecT>
+__device__ __forceinline__ uint32_t wg_count(uint32_t src, uint32_t c0, uint32_t c1, uint32_t k, int lane) {
+  constexpr uint32_t E = WGTile<RecT>::E, SC = WGTile<RecT>::SC, RB = sizeof(RecT);
+  const uint32_t sA = src + lane * (E * RB);
+  uint32_t acc = 0;
+#pragma unroll 4
+  for (uint32_t c = c0; c < c1; c++) {
+    if constexpr (RB == 1) {
+      const uint2 x = lds64(sA + c * (SC * RB));
+      acc += ((x.x >> k) & 0x01010101u) + ((x.y >> k) & 0x01010101u);
+    } else if constexpr (RB == 2) {
+      const uint4 x = lds128(sA + c * (SC * RB));
+      acc += ((x.x >> k) & 0x00010001u) + ((x.y >> k) & 0x00010001u) + ((x.z >> k) & 0x00010001u) +
+             ((x.w >> k) & 0x00010001u);
+    } else {
+      const uint2 x = lds64(sA + c * (SC * RB));
+      acc += ((x.x >> k) & 1u) + ((x.y >> k) & 1u);
+    }
+  }
+  if constexpr (RB == 1) acc = (acc * 0x01010101u) >> 24;  // bytes <= 2 per superchunk: no overflow
+  else if constexpr (RB == 2) acc = (acc + (acc >> 16)) & 0xffffu;
+  return __reduce_add_sync(FULL, acc);
+}
+
+// ones of the level before sub-tile position p (p <= padded length)
+__device__ __forceinline__ uint32_t wg_rank1(const uint32_t *LBw, const uint16_t *RP, uint32_t p) {
+  const uint32_t w = p >> 5;
+  return RP[w] + __popc(LBw[w] & ((1u << (p & 31u)) - 1u));
+}
+
+// bits [pos, pos + nb) of the sub-tile bitmap (u32 words), nb <= 64, LSB first
+__device__ __forceinline__ uint64_t lb_bits(const uint32_t *LBw, uint32_t pos, uint32_t nb) {
+  const uint32_t w = pos >> 5, sh = pos & 31u;
+  const uint32_t x0 = LBw[w], x1 = LBw[w + 1], x2 = LBw[w + 2];
+  const uint64_t v = ((uint64_t)__funnelshift_r(x1, x2, sh) << 32) | __funnelshift_r(x0, x1, sh);
+  return nb >= 64 ? v : v & ((1ull << nb) - 1ull);
+}
+
+#ifndef WT_WG_INLANE
+#define WT_WG_INLANE 3
+#endif
+// One run (one lane): sub-tile bitmap bits [ls, ls+cnt) -> global bits
+// [G, G+cnt) of B (cnt > 0).  The first word takes the carried bits of the
+// slot; it is OR-ed atomically when its low bits belong to another chain or
+// node, stored otherwise; a partial last word is carried to the next sub-tile
+// of the chain.  Interior words are stored here when few, else their count is
+// returned for the cooperative pass.
+__device__ __forceinline__ uint32_t wg_run(unsigned long long &cw, uint8_t &cf, const uint32_t *LBw, uint64_t *B,
+                                           uint64_t n, uint32_t G, uint32_t ls, uint32_t cnt) {
+  const uint32_t g0 = G & 63u;
+  const uint64_t e = (uint64_t)G + cnt;
+  const uint32_t gw0 = G >> 6, gwl = (uint32_t)((e - 1) >> 6);
+  const uint32_t hb = min(cnt, 64u - g0);
+  uint64_t head = lb_bits(LBw, ls, hb) << g0;
+  bool shared;
+  const uint32_t f = cf;
+  if (f & CF_VALID) {
+    head |= cw;
+    shared = (f & CF_SHARED) != 0;
+  } else {
+    shared = g0 != 0;
+  }
+  const uint64_t wend0 = (uint64_t)gw0 * 64 + 64 < n ? (uint64_t)gw0 * 64 + 64 : n;
+  if (gw0 == gwl && e < wend0) {  // the word stays open: carry it
+    cw = head;
+    cf = CF_VALID | (shared ? CF_SHARED : 0);
+    return 0u;
+  }
+  if (shared) atomicOr(reinterpret_cast<unsigned long long *>(&B[gw0]), (unsigned long long)head);
+  else B[gw0] = head;
+  cf = 0;
+  if (gw0 == gwl) return 0u;
+  const uint32_t tb = (uint32_t)(e - (uint64_t)gwl * 64);  // 1..64 bits in the last word
+  const uint64_t tail = lb_bits(LBw, ls + cnt - tb, tb);
+  const uint64_t wendl = (uint64_t)gwl * 64 + 64 < n ? (uint64_t)gwl * 64 + 64 : n;
+  if (e >= wendl) {
+    B[gwl] = tail;
+  } else {
+    cw = tail;
+    cf = CF_VALID;
+  }
+  const uint32_t ni = gwl - gw0 - 1;
+  if (ni <= WT_WG_INLANE) {
+    for (uint32_t w = 0; w < ni; w++) B[gw0 + 1 + w] = lb_bits(LBw, ls + hb + 64u * w, 64);
+    return 0u;
+  }
+  return ni;
+}
+
+// ---- TMA bulk copy (cp.async.bulk) of the raw input of one sub-tile ----
+__device__ __forceinline__ void bar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// lane 0: the aligned 16-byte cover of [src, src + bytes) into dst; returns the head offset
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + bytes + 15) & ~(uintptr_t)15;
+  const uint32_t sz = (uint32_t)(a1 - a0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(sz) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(a0), "r"(sz), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  }
+}
+
+// raw 32-bit words of one 16-byte record group from the staging buffer:
+// in[0 .. 4*NV) = bytes [h + 16*NV*g, +16*NV) (h = head offset < 16, uniform)
+template <uint32_t NV>
+__device__ __forceinline__ void stage_words(const uint8_t *stg, uint32_t g, uint32_t h, uint32_t *in) {
+  const uint4 *V = reinterpret_cast<const uint4 *>(stg) + NV * g;
+  uint32_t raw[4 * NV + 4];
+#pragma unroll
+  for (uint32_t q = 0; q < NV; q++) {
+    const uint4 u = V[q];
+    raw[4 * q] = u.x; raw[4 * q + 1] = u.y; raw[4 * q + 2] = u.z; raw[4 * q + 3] = u.w;
+  }
+  if (h == 0) {
+#pragma unroll
+    for (uint32_t q = 0; q < 4 * NV; q++) in[q] = raw[q];
+    return;
+  }
+  {
+    const uint4 u = V[NV];
+    raw[4 * NV] = u.x; raw[4 * NV + 1] = u.y; raw[4 * NV + 2] = u.z; raw[4 * NV + 3] = u.w;
+  }
+  const uint32_t hb = 8u * (h & 3u);
+#define WG_SHIFT(H)                                                                                             \
+  case H:                                                                                                       \
+    _Pragma("unroll") for (uint32_t q = 0; q < 4 * NV; q++) in[q] = __funnelshift_r(raw[q + H], raw[q + H + 1], hb); \
+    break;
+  switch (h >> 2) { WG_SHIFT(0) WG_SHIFT(1) WG_SHIFT(2) WG_SHIFT(3) }
+#undef WG_SHIFT
+}
+
+template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
+__global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
+  using SM = WGSmem<InT, RecT, HAS_OUT>;
+  constexpr uint32_t T = SM::T, SC = WGTile<RecT>::SC, SPW = WGTile<RecT>::SPW, RB = sizeof(RecT),
+                     IB = sizeof(InT);
+  constexpr uint32_t PER = 16 / RB, NV = PER * IB / 16;  // records per 16-byte group, input uint4 per group
+  constexpr uint32_t NT = CT_WARPS * 32;
+  extern __shared__ __align__(16) uint8_t wg_raw[];
+  SM &s = *reinterpret_cast<SM *>(wg_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (ld_relaxed(p.err)) return;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t tau = p.tau, pbits = p.pbits, kb = tau + pbits;
+  const uint32_t ndig = 1u << tau, dmask = ndig - 1u;
+  const uint32_t pmask = pbits >= 32 ? 0xffffffffu : (1u << pbits) - 1u;
+  const uint32_t nchains = p.counts[0];
+  const InT *keys = reinterpret_cast<const InT *>(p.keys_in);
+  const uint32_t bar = smem_u32(&s.bar), stg = smem_u32(s.stage);
+  // thread 0: claim a chain and start the bulk copy of its first tile
+  auto claim = [&]() {
+    const uint32_t c = atomicAdd(p.chain_counter, 1u);
+    if (c < nchains) {
+      const uint32_t b = p.chain_begin[c], e = p.chain_end[c];
+      bulk_load(stg, keys + b, min(e - b, T) * IB, bar);
+    }
+    return c;
+  };
+  if (tid == 0) {
+    bar_init(bar);
+    s.chain = claim();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  uint32_t c = s.chain;
+
+  while (c < nchains) {
+    // ---- chain setup: running positions of every class slot and digit ----
+    const uint32_t row = p.chain_row[c];
+    const uint32_t cbeg = p.chain_begin[c], cend = p.chain_end[c];
+    const uint32_t rstart = p.row_start[row];
+    const uint32_t *Cg = p.Cseg + (uint64_t)row * (ndig + 1);
+    uint32_t *X = reinterpret_cast<uint32_t *>(s.CW);  // scratch until the carries start
+    if (warp == 0) {
+      const uint32_t cfirst = p.row_first[row];
+      // X[d] = exclusive scan over digits of the same-row elements ahead of the chain
+      uint32_t v[8], sum = 0;
+      const uint32_t per = (ndig + 31) >> 5, lo = min(lane * per, ndig), hi = min(lo + per, ndig);
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const uint32_t d = lo + i;
+        v[i] = (d < hi) ? p.E[(uint64_t)d * p.estride + c] - p.E[(uint64_t)d * p.estride + cfirst] : 0u;
+        sum += v[i];
+      }
+      const uint32_t incl = warp_incl_scan(sum, lane);
+      uint32_t run = incl - sum;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const uint32_t d = lo + i;
+        if (d < hi) {
+          if constexpr (HAS_OUT) s.kpos[d] = rstart + Cg[d] + v[i];
+          X[d] = run;
+          run += v[i];
+        }
+      }
+      if (lane == 31) X[ndig] = incl;
+    }
+    __syncthreads();
+    // slot 2^k + r, class q = rev_k(r): rstart + Cseg[q << (tau-k)] + (X[(q+1) << (tau-k)] - X[q << (tau-k)])
+    for (uint32_t slot = 1 + tid; slot < ndig; slot += NT) {
+      const uint32_t k = 31 - __clz(slot), r = slot - (1u << k);
+      const uint32_t q = rev_bits(r, k), sh = tau - k;
+      s.pos[slot] = rstart + Cg[q << sh] + (X[(q + 1) << sh] - X[q << sh]);
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < 256; i += NT) s.CF[i] = 0;
+
+    for (uint64_t start64 = cbeg; start64 < cend; start64 += T) {
+      const uint32_t start = (uint32_t)start64;
+      const uint32_t rem = cend - start;
+      const uint32_t len = rem < T ? rem : T;
+      const uint32_t nsc = (len + SC - 1) / SC, ntot = nsc * SC;
+      const uint32_t c0 = min((uint32_t)warp * SPW, nsc), c1 = min(c0 + SPW, nsc);  // this warp's quarter
+
+      // ---- 1. records (bit-reversed keys) from the staged input + ones of bit 0 per quarter ----
+      bar_wait(bar, phase);
+      phase ^= 1u;
+      {
+        const uint32_t h = (uint32_t)(reinterpret_cast<uintptr_t>(keys + start) & 15u);
+        RecT *R = s.rec[0];
+        uint32_t ones0 = 0;
+        for (uint32_t g = c0 * (SC / PER) + lane; g < c1 * (SC / PER); g += 32) {
+          const uint32_t i0 = g * PER;
+          uint32_t in[4 * NV], w[4];
+          stage_words<NV>(s.stage, g, h, in);
+          if constexpr (IB == 1 && RB == 1) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              uint32_t x = __byte_perm(__brev(in[q]), 0, 0x0123);  // every byte bit-reversed
+              if (kb < 8) x = (x >> (8u - kb)) & (((1u << kb) - 1u) * 0x01010101u);
+              w[q] = x;
+            }
+          } else if constexpr (IB == 4 && RB == 2) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              uint32_t x = __byte_perm(__brev(in[2 * q]), __brev(in[2 * q + 1]), 0x7632);
+              if (kb < 16) x = (x >> (16u - kb)) & (((1u << kb) - 1u) * 0x00010001u);
+              w[q] = x;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++) w[q] = 0u;
+#pragma unroll
+            for (uint32_t e = 0; e < PER; e++) {
+              uint32_t key;
+              if constexpr (IB == 1) key = (in[e >> 2] >> (8 * (e & 3))) & 0xffu;
+              else if constexpr (IB == 2) key = (in[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+              else key = in[e];
+              w[(e * RB) >> 2] |= (__brev(key) >> (32u - kb)) << (8u * ((e * RB) & 3u));
+            }
+          }
+          if (i0 + PER > len) {  // padding records (all ones: a one at every level, they stay last)
+#pragma unroll
+            for (uint32_t e = 0; e < PER; e++) {
+              if (i0 + e >= len) {
+                if constexpr (RB == 4) w[e] = 0xffffffffu;
+                else w[(e * RB) >> 2] |= ((1u << (8 * RB)) - 1u) << (8u * ((e * RB) & 3u));
+              }
+            }
+          }
+          if constexpr (RB == 1) {
+            ones0 += __popc((w[0] & 0x01010101u)) + __popc(w[1] & 0x01010101u) + __popc(w[2] & 0x01010101u) +
+                     __popc(w[3] & 0x01010101u);
+          } else if constexpr (RB == 2) {
+            ones0 += __popc((w[0] & 0x00010001u)) + __popc(w[1] & 0x00010001u) + __popc(w[2] & 0x00010001u) +
+                     __popc(w[3] & 0x00010001u);
+          } else {
+            ones0 += (w[0] & 1u) + (w[1] & 1u) + (w[2] & 1u) + (w[3] & 1u);
+          }
+          *reinterpret_cast<uint4 *>(R + i0) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        ones0 = __reduce_add_sync(FULL, ones0);
+        if (lane == 0) s.onesW[warp] = ones0;
+      }
+      if (tid == 0) {
+        s.C[1] = (uint16_t)len;  // slot 1: the one class of level 0
+        s.S[1] = 0;
+      }
+      __syncthreads();
+      // the staging buffer is free: prefetch the next tile of the chain, or the next chain's first
+      if (tid == 0) {
+        if (start64 + T < cend) bulk_load(stg, keys + start + T, min(cend - (start + T), T) * IB, bar);
+        else s.cnext = claim();
+      }
+
+      // ---- 2. tau levels of splits (bitmaps and word ranks kept per level) ----
+      for (uint32_t k = 0; k < tau; k++) {
+        uint32_t before = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < CT_WARPS; w++) {
+          const uint32_t o = s.onesW[w];
+          before += w < warp ? o : 0u;
+          tot += o;
+        }
+        const uint32_t Z = ntot - tot;  // zeros of bit k (padding records are ones)
+        if (tid == 0) s.Zs[k] = Z;
+        const uint32_t src = smem_u32(s.rec[k & 1u]), dst = smem_u32(s.rec[(k & 1u) ^ 1u]);
+        const bool move = HAS_OUT || k + 1 < tau;
+        if (c0 < c1) {
+          if (move) wg_split<RecT, true>(s.LB[k], s.RP[k], src, dst, c0, c1, nsc, k, Z, before, lane, lt);
+          else wg_split<RecT, false>(s.LB[k], s.RP[k], src, dst, c0, c1, nsc, k, Z, before, lane, lt);
+        }
+        __syncthreads();
+        if (k + 1 < tau) {
+          const uint32_t o = c0 < c1 ? wg_count<RecT>(dst, c0, c1, k + 1, lane) : 0u;
+          if (lane == 0) s.onesW[warp] = o;
+          __syncthreads();
+        }
+      }
+
+      // ---- 3. classes of every level: M_{k+1} = the zeros of M_k, then its ones ----
+      // slot 2^k + r holds class r of level k (r = reversed k-bit prefix)
+#ifdef WT_WG_DIAG_NORUNS
+      const uint32_t kmax = 0;
+#else
+      const uint32_t kmax = HAS_OUT ? tau : tau - 1u;  // deepest level whose classes are needed
+#endif
+      auto classes_of = [&](uint32_t k) {
+        const uint32_t nk = 1u << k;
+        const uint32_t *LBw = reinterpret_cast<const uint32_t *>(s.LB[k]);
+        const uint32_t Zk = s.Zs[k];
+        for (uint32_t r = tid; r < nk; r += NT) {
+          const uint32_t st = s.S[nk + r], cn = s.C[nk + r];
+          const uint32_t a = wg_rank1(LBw, s.RP[k], st), b = wg_rank1(LBw, s.RP[k], st + cn);
+          s.C[2 * nk + r] = (uint16_t)(cn - (b - a));
+          s.C[3 * nk + r] = (uint16_t)(b - a);
+          s.S[2 * nk + r] = (uint16_t)(st - a);
+          s.S[3 * nk + r] = (uint16_t)(Zk + a);
+        }
+      };
+      if (warp == 0) {  // levels with <= 16 classes: warp 0 alone (warp-synchronous)
+        for (uint32_t k = 0; k < min(kmax, 5u); k++) {
+          classes_of(k);
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (uint32_t k = 5; k < kmax; k++) {
+        classes_of(k);
+        __syncthreads();
+      }
+
+      // ---- 4. runs of every level (thread per class), long runs' interior words by the warp ----
+#ifdef WT_WG_DIAG_NORUNS
+      for (uint32_t s0 = 1; s0 < 0; s0 += NT) {
+#else
+      for (uint32_t s0 = 1; s0 < ndig; s0 += NT) {
+#endif
+        const uint32_t slot = s0 + tid;
+        uint32_t ni = 0, gwA = 0, lsA = 0, kk = 0;
+        if (slot < ndig) {
+          const uint32_t cn = s.C[slot];
+          if (cn) {
+            kk = 31 - __clz(slot);
+            const uint32_t G = s.pos[slot], ls = s.S[slot];
+            uint64_t *B = p.bits + (uint64_t)(p.l0 + kk) * p.wpl;
+            ni = wg_run(s.CW[slot], s.CF[slot], reinterpret_cast<const uint32_t *>(s.LB[kk]), B, p.n, G, ls, cn);
+            gwA = (G >> 6) + 1;
+            lsA = ls + min(cn, 64u - (G & 63u));
+            s.pos[slot] = G + cn;
+          }
+        }
+        uint32_t m = __ballot_sync(FULL, ni != 0);
+        while (m) {
+          const int src_l = __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t g = __shfl_sync(FULL, gwA, src_l), l0 = __shfl_sync(FULL, lsA, src_l),
+                         nn = __shfl_sync(FULL, ni, src_l), k2 = __shfl_sync(FULL, kk, src_l);
+          uint64_t *B = p.bits + (uint64_t)(p.l0 + k2) * p.wpl;
+          const uint32_t *LBw = reinterpret_cast<const uint32_t *>(s.LB[k2]);
+          for (uint32_t w = lane; w < nn; w += 32) B[g + w] = lb_bits(LBw, l0 + 64u * w, 64);
+        }
+      }
+
+      // ---- 5. narrowed keys at their S_{l0+tau} position (A6) ----
+#ifdef WT_WG_DIAG_NORUNS
+      if constexpr (false) {
+#else
+      if constexpr (HAS_OUT) {
+#endif
+        const uint32_t fin = tau & 1u;
+        uint32_t *KB = reinterpret_cast<uint32_t *>(s.rec[fin ^ 1u]);  // free after the last split
+        for (uint32_t r = tid; r < ndig; r += NT) {
+          const uint32_t d = rev_bits(r, tau);
+          const uint32_t kp = s.kpos[d];
+          KB[r] = kp - s.S[ndig + r];
+          s.kpos[d] = kp + s.C[ndig + r];
+        }
+        __syncthreads();
+        OutT *ko = reinterpret_cast<OutT *>(p.keys_out);
+        const RecT *R = s.rec[fin];
+#pragma unroll 4
+        for (uint32_t i = tid; i < len; i += NT) {
+          const uint32_t r = R[i];
+          const uint32_t key = __brev(r) >> (32u - kb);
+          ko[KB[r & dmask] + i] = (OutT)(key & pmask);
+        }
+      }
+      __syncthreads();
+    }
+    // ---- chain end: flush carried words (shared with the next chain or row) ----
+    for (uint32_t slot = 1 + tid; slot < ndig; slot += NT) {
+      if (s.CF[slot] & CF_VALID) {
+        uint64_t *B = p.bits + (uint64_t)(p.l0 + (31 - __clz(slot))) * p.wpl;
+        atomicOr(reinterpret_cast<unsigned long long *>(&B[s.pos[slot] >> 6]), s.CW[slot]);
+      }
+    }
+    __syncthreads();
+    c = s.cnext;
+    __syncthreads();
+  }
+}
+
+}  // namespace wtb

@@ -4,6 +4,7 @@ import csv, io, os, re, subprocess, sys, tempfile
 from collections import Counter
 rep, which, mangled = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+DUMP = os.environ.get("DUMP")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 lib = os.environ.get("WT_LIB_PATH", os.path.join(ROOT, "paper_1407_8142_b200", "libwt_b200.so"))
 td = tempfile.mkdtemp()
@@ -53,3 +54,6 @@ for (f, ln), v in cnt.most_common(top):
         srcs[f] = open(p).read().splitlines() if os.path.exists(p) else []
     text = srcs[f][ln - 1].strip()[:80] if 0 < ln <= len(srcs[f]) else ""
     print(f"{100*v/tot:5.1f}% {100*smp[(f,ln)]/max(1,sum(smp.values())):5.1f}%s  {f}:{ln:<4d} {text}")
+if DUMP:  # per-line counts as JSON for phase aggregation
+    import json
+    json.dump({f"{f}:{ln}": [v, smp[(f, ln)]] for (f, ln), v in cnt.items()}, open(DUMP, "w"))

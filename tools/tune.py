@@ -8,22 +8,32 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
-    "base": ["WT_GMINB=5", "WT_GTT=8192"],
-    "redux": ["WT_GMINB=5", "WT_GTT=8192", "WT_CNT_REDUX=1"],
+    "tb8k_w4": ["WT_CT_TB=8192", "WT_CT_WARPS=4"],
+    "tb16k_w4": ["WT_CT_TB=16384", "WT_CT_WARPS=4"],
+    "tb16k_w8": ["WT_CT_TB=16384", "WT_CT_WARPS=8"],
+    "tb8k_w8": ["WT_CT_TB=8192", "WT_CT_WARPS=8"],
+    "tb8k_w2": ["WT_CT_TB=8192", "WT_CT_WARPS=2"],
 }
-CPW = os.environ.get("TUNE_CPW", "3").split(",")
+if os.environ.get("TUNE_ONLY"):
+    VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
+CPW = os.environ.get("TUNE_CPW", "4").split(",")
 if sys.argv[1] == "build":
     from paper_1407_8142_b200 import _build
     os.makedirs(VDIR, exist_ok=True)
-    for name, defs in VARIANTS.items():
+    from concurrent.futures import ThreadPoolExecutor
+    def one(item):
+        name, defs = item
         _build.build(force=True, defines=defs, out=os.path.join(VDIR, f"lib_{name}.so"))
-        print("built", name)
+        return name
+    with ThreadPoolExecutor(len(VARIANTS)) as ex:
+        for name in ex.map(one, VARIANTS.items()):
+            print("built", name)
 else:
     cfgs = sys.argv[2:] or ["4"]
     for name in VARIANTS:
       for cpw in CPW:
         env = dict(os.environ, WT_LIB_PATH=os.path.join(VDIR, f"lib_{name}.so"), WT_CHAINS_PER_WARP=cpw)
-        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "probe.py"), *cfgs],
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "kprof.py"), *cfgs],
                              capture_output=True, text=True, env=env, timeout=600)
         lines = [l for l in out.stdout.splitlines() if l.startswith("cfg") or "k_group" in l]
         print(f"== {name} cpw={cpw}")
