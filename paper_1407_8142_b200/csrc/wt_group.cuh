@@ -52,11 +52,14 @@ struct GroupParams {
   const uint32_t *E;          // E[d][c]: same-row elements with digit d ahead of chain c (+ row offset)
   uint32_t estride;
   const uint32_t *Cseg;       // [row][ndig + 1]
+  const uint32_t *V;          // [chain][256]: same-row elements with digit d ahead of the chain (k_wgroup)
   const uint32_t *row_start;
   uint32_t *chain_counter;
   uint64_t *bits;
   uint64_t wpl;
   uint32_t *err;
+  uint32_t *blkcnt;  // [level][bpl]: ones per 512-bit block, accumulated by k_wgroup (fused A7)
+  uint64_t bpl;
 };
 
 #ifdef WT_PHASES

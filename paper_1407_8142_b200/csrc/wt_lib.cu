@@ -161,7 +161,7 @@ struct GroupBufs {
   void *keys_out = nullptr;
   uint32_t *chain_begin = nullptr, *chain_end = nullptr, *chain_row = nullptr;
   uint32_t *row_first = nullptr, *row_start = nullptr, *row_key = nullptr;
-  uint32_t *E = nullptr, *Cseg = nullptr;
+  uint32_t *E = nullptr, *Cseg = nullptr, *V = nullptr;
   uint32_t *rowcnt = nullptr, *bsum = nullptr;
   uint32_t nblk = 0;
   uint32_t *counts = nullptr;  // [0] chains, [1] rows, [2] chain claim counter
@@ -175,6 +175,7 @@ struct GroupBufs {
     if (!local) {
       E = A.alloc<uint32_t>((uint64_t)ndig * (max_chains + 1), false);
       Cseg = A.alloc<uint32_t>(max_rows * (ndig + 1), false);
+      if (!use_old_group()) V = A.alloc<uint32_t>((uint64_t)max_chains * 256, false);
     }
     const uint64_t nunits = local ? nbatch : max_rows;  // node counts per batch (local) or row
     nblk = (uint32_t)((nunits + SCAN_BLK - 1) / SCAN_BLK);
@@ -296,6 +297,10 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   uint32_t *err = A.alloc<uint32_t>(4, false);
   uint32_t *ncount = A.alloc<uint32_t>(L + 1, false);
   uint64_t *suptot = A.alloc<uint64_t>(L * NSD, false);
+  // fused A7: block popcounts accumulated by the k_wgroup passes (chain-mode groups)
+  bool any_chain = false;
+  for (uint32_t g = 0; g < NG; g++) any_chain |= !G[g].local;
+  uint32_t *blkcnt = (any_chain && !use_old_group() && n) ? A.alloc<uint32_t>((uint64_t)L * BPL, false) : nullptr;
   const uint32_t small_tiles = small ? (uint32_t)((n + SMALL_TILE - 1) / SMALL_TILE) : 0u;
   uint32_t *small_zc = small ? A.alloc<uint32_t>(small_tiles, false) : nullptr;
   uint64_t *small_tot = small ? A.alloc<uint64_t>(1, false) : nullptr;
@@ -321,6 +326,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   chk(cudaMemsetAsync(err, 0, 4 * sizeof(uint32_t), s));
   chk(cudaMemsetAsync(t->level_node_ptr, 0, (L + 1) * sizeof(uint64_t), s));
   if (L && n) chk(cudaMemsetAsync(t->bits, 0, L * WPL * sizeof(uint64_t), s));
+  if (blkcnt) chk(cudaMemsetAsync(blkcnt, 0, (uint64_t)L * BPL * sizeof(uint32_t), s));
   for (uint32_t g = 0; g < NG; g++) chk(cudaMemsetAsync(G[g].counts, 0, 4 * sizeof(uint32_t), s));
 
   // A7 per level group, on the side stream once the group's bitmaps are final
@@ -501,6 +507,11 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     k_row_scan<<<(unsigned)((gb.max_rows * 32 + 255) / 256), 256, 0, s>>>(gb.E, stride, gb.row_first, gb.counts,
                                                                           gb.ndig, gb.Cseg, err);
     chk(cudaGetLastError());
+    if (gb.V)
+      k_chain_vec<<<(unsigned)((gb.max_chains * 32 + 255) / 256), 256, 0, s>>>(gb.E, stride, gb.chain_row,
+                                                                              gb.row_first, gb.counts, gb.ndig, gb.V,
+                                                                              err);
+    chk(cudaGetLastError());
     rec.end();
     // ---- A4: node table of this group's levels l0+k_lo .. l0+k_lo+nk-1 ----
     if (gb.nk && g == 0) {
@@ -545,11 +556,14 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     gp.E = gb.E;
     gp.estride = stride;
     gp.Cseg = gb.Cseg;
+    gp.V = gb.V;
     gp.row_start = gb.row_start;
     gp.chain_counter = gb.counts + 2;
     gp.bits = t->bits;
     gp.wpl = WPL;
     gp.err = err;
+    gp.blkcnt = blkcnt;
+    gp.bpl = BPL;
     const bool has_out = g + 1 < NG;
     char name[32];
     snprintf(name, sizeof(name), "k_group%u", g);
@@ -557,7 +571,19 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     gb.gl.kern<<<gb.gl.grid, gb.gl.threads, gb.gl.smem, s>>>(gp);
     chk(cudaGetLastError());
     rec.end();
-    rank_levels(gb.l0, gb.tau);
+    if (blkcnt) {
+      // fused A7: the pass accumulated the block popcounts; scan them per superblock
+      if (NSD) {
+        rec.begin("k_rank_counts", (uint64_t)gb.tau * (BPL * 4 + BPL * 2 + NSD * 8));
+        const uint64_t warps = (uint64_t)gb.tau * NSD;
+        k_rank_counts<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(blkcnt, BPL, NSD, gb.l0, gb.tau,
+                                                                            t->rank_block, suptot, err);
+        chk(cudaGetLastError());
+        rec.end();
+      }
+    } else {
+      rank_levels(gb.l0, gb.tau);
+    }
     keys_in = gb.keys_out;
   }
 

@@ -169,6 +169,22 @@ static __global__ void __launch_bounds__(1024) k_chain_scan(uint32_t *__restrict
   }
 }
 
+// V[c][d] = E[d][c] - E[d][first chain of c's row]: the chain's starting digit
+// counts inside its row, chain-major (one 1 KB vector per chain, bulk-copied by
+// k_wgroup together with the chain's first tile).  One warp per chain.
+static __global__ void k_chain_vec(const uint32_t *__restrict__ E, uint32_t stride, const uint32_t *__restrict__ chain_row,
+                                   const uint32_t *__restrict__ row_first, const uint32_t *__restrict__ counts,
+                                   uint32_t ndig, uint32_t *__restrict__ V, const uint32_t *err) {
+  if (*err) return;
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= counts[0]) return;
+  const uint32_t f = row_first[chain_row[c]];
+  uint32_t *out = V + (uint64_t)c * 256;
+  for (uint32_t d = lane; d < 256; d += 32)
+    out[d] = d < ndig ? E[(uint64_t)d * stride + c] - E[(uint64_t)d * stride + f] : 0u;
+}
+
 // Cseg[r][0..ndig] = exclusive scan over d of the row's digit totals
 // E[d][row_first[r+1]] - E[d][row_first[r]].  One warp per row.
 static __global__ void k_row_scan(const uint32_t *__restrict__ E, uint32_t stride, const uint32_t *__restrict__ row_first,

@@ -54,6 +54,38 @@ static __global__ void k_rank_local(const uint64_t *__restrict__ bits, uint64_t 
   if (lane == 31) suptot[(uint64_t)l * nsup_data + s] = incl;
 }
 
+// A7 finalize from the block popcounts the group pass accumulated (fused A7):
+// blkcnt[l*bpl + b] = ones of block b of level l.  One warp per (level, superblock).
+static __global__ void k_rank_counts(const uint32_t *__restrict__ blkcnt, uint64_t bpl, uint64_t nsup_data,
+                                     uint32_t lbeg, uint32_t nl, uint16_t *__restrict__ rank_block,
+                                     uint64_t *__restrict__ suptot, const uint32_t *err) {
+  if (*err) return;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= (uint64_t)nl * nsup_data) return;
+  const uint32_t l = lbeg + (uint32_t)(gw / nsup_data);
+  const uint64_t s = gw % nsup_data;
+  const uint64_t b0 = s * 128 + lane * 4;
+  uint32_t v[4] = {0, 0, 0, 0}, sum = 0;
+  if (b0 + 4 <= bpl && (((uint64_t)l * bpl + b0) & 3) == 0) {
+    const uint4 q = *reinterpret_cast<const uint4 *>(blkcnt + (uint64_t)l * bpl + b0);
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; i++) v[i] = (b0 + i < bpl) ? blkcnt[(uint64_t)l * bpl + b0 + i] : 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) sum += v[i];
+  const uint32_t incl = warp_incl_scan(sum, lane);
+  uint32_t run = incl - sum;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    if (b0 + i < bpl) rank_block[(uint64_t)l * bpl + b0 + i] = (uint16_t)run;
+    run += v[i];
+  }
+  if (lane == 31) suptot[(uint64_t)l * nsup_data + s] = incl;
+}
+
 static __global__ void __launch_bounds__(1024) k_rank_super(const uint64_t *__restrict__ suptot, uint64_t nsup_data,
                                                     uint64_t spl, uint64_t *__restrict__ rank_super,
                                                     const uint32_t *err) {

@@ -77,6 +77,7 @@ struct WGSmem {
   alignas(16) uint8_t stage[T * sizeof(InT) + 32];  // raw input of the next tile (TMA bulk copy)
   alignas(16) uint8_t LB[TAU_MAX][LBB];  // level bitmaps of the tile (M_k order)
   alignas(16) uint16_t RP[TAU_MAX][RPW]; // ones of the level before each 32-bit word of LB
+  alignas(16) uint32_t V[256];           // chain's starting digit counts (bulk copy, next chain's)
   alignas(16) uint32_t pos[256];         // running global bit position of slot 2^k + r
   alignas(16) uint32_t kpos[HAS_OUT ? 256 : 1];  // running key position per (true) digit
   alignas(16) unsigned long long CW[256];        // carried partial word per slot (chain setup: scratch)
@@ -270,40 +271,57 @@ __device__ __forceinline__ uint32_t wg_rank1(const uint32_t *LBw, const uint16_t
   return RP[w] + __popc(LBw[w] & ((1u << (p & 31u)) - 1u));
 }
 
-// bits [pos, pos + nb) of the sub-tile bitmap (u32 words), nb <= 64, LSB first
+// bits [pos, pos + nb) of a tile bitmap (u32 words), 1 <= nb <= 64, LSB first
 __device__ __forceinline__ uint64_t lb_bits(const uint32_t *LBw, uint32_t pos, uint32_t nb) {
   const uint32_t w = pos >> 5, sh = pos & 31u;
   const uint32_t x0 = LBw[w], x1 = LBw[w + 1], x2 = LBw[w + 2];
-  const uint64_t v = ((uint64_t)__funnelshift_r(x1, x2, sh) << 32) | __funnelshift_r(x0, x1, sh);
-  return nb >= 64 ? v : v & ((1ull << nb) - 1ull);
+  uint32_t lo = __funnelshift_r(x0, x1, sh), hi = __funnelshift_r(x1, x2, sh);
+  if (nb < 32) {
+    lo &= (1u << nb) - 1u;
+    hi = 0;
+  } else if (nb < 64) {
+    hi &= (1u << (nb - 32)) - 1u;
+  }
+  return ((uint64_t)hi << 32) | lo;
 }
 
 #ifndef WT_WG_INLANE
 #define WT_WG_INLANE 3
 #endif
-// One run (one lane): sub-tile bitmap bits [ls, ls+cnt) -> global bits
-// [G, G+cnt) of B (cnt > 0).  The first word takes the carried bits of the
-// slot; it is OR-ed atomically when its low bits belong to another chain or
-// node, stored otherwise; a partial last word is carried to the next sub-tile
-// of the chain.  Interior words are stored here when few, else their count is
-// returned for the cooperative pass.
+// One run (one thread): tile bitmap bits [ls, ls+cnt) -> global bits
+// [G, G+cnt) of B (cnt > 0, G + cnt <= n < 2^32).  The first word takes the
+// carried bits of the slot; it is OR-ed atomically when its low bits belong to
+// another chain or node, stored otherwise; an unfinished last word (the run
+// ends inside it before n) is carried to the next tile of the chain.  Interior
+// words are stored here when few, else their count is returned for the
+// cooperative pass.
+// fused A7: a run [G, G+cnt) placed from tile bits
+// [ls, ls+cnt) adds, to every 512-bit block it overlaps, the ones of the
+// overlap -- two rank queries on the tile bitmap (bits are counted where they
+// come from, independent of when their word is committed)
+__device__ __forceinline__ void run_blocks(uint32_t *bc, const uint32_t *LBw, const uint16_t *RP, uint32_t G,
+                                           uint32_t ls, uint32_t cnt, uint32_t b_lo, uint32_t b_hi, uint32_t step) {
+  const uint32_t e = G + cnt;
+  for (uint32_t b = b_lo; b <= b_hi; b += step) {
+    const uint32_t lo = max(G, b << 9), hi = min(e, (b << 9) + 512u);
+    const uint32_t c = wg_rank1(LBw, RP, ls + (hi - G)) - wg_rank1(LBw, RP, ls + (lo - G));
+    if (c) atomicAdd(bc + b, c);
+  }
+}
 __device__ __forceinline__ uint32_t wg_run(unsigned long long &cw, uint8_t &cf, const uint32_t *LBw, uint64_t *B,
-                                           uint64_t n, uint32_t G, uint32_t ls, uint32_t cnt) {
-  const uint32_t g0 = G & 63u;
-  const uint64_t e = (uint64_t)G + cnt;
-  const uint32_t gw0 = G >> 6, gwl = (uint32_t)((e - 1) >> 6);
+                                           uint32_t n32, uint32_t G, uint32_t ls, uint32_t cnt) {
+  const uint32_t g0 = G & 63u, e = G + cnt;
+  const uint32_t gw0 = G >> 6, gwl = (e - 1u) >> 6;
   const uint32_t hb = min(cnt, 64u - g0);
   uint64_t head = lb_bits(LBw, ls, hb) << g0;
-  bool shared;
   const uint32_t f = cf;
+  bool shared = g0 != 0;
   if (f & CF_VALID) {
     head |= cw;
     shared = (f & CF_SHARED) != 0;
-  } else {
-    shared = g0 != 0;
   }
-  const uint64_t wend0 = (uint64_t)gw0 * 64 + 64 < n ? (uint64_t)gw0 * 64 + 64 : n;
-  if (gw0 == gwl && e < wend0) {  // the word stays open: carry it
+  const bool open_end = (e & 63u) != 0 && e != n32;  // the run's last word is unfinished
+  if (gw0 == gwl && open_end) {
     cw = head;
     cf = CF_VALID | (shared ? CF_SHARED : 0);
     return 0u;
@@ -312,18 +330,17 @@ __device__ __forceinline__ uint32_t wg_run(unsigned long long &cw, uint8_t &cf, 
   else B[gw0] = head;
   cf = 0;
   if (gw0 == gwl) return 0u;
-  const uint32_t tb = (uint32_t)(e - (uint64_t)gwl * 64);  // 1..64 bits in the last word
+  const uint32_t tb = e - (gwl << 6);  // 1..64 bits in the last word
   const uint64_t tail = lb_bits(LBw, ls + cnt - tb, tb);
-  const uint64_t wendl = (uint64_t)gwl * 64 + 64 < n ? (uint64_t)gwl * 64 + 64 : n;
-  if (e >= wendl) {
-    B[gwl] = tail;
-  } else {
+  if (open_end) {
     cw = tail;
     cf = CF_VALID;
+  } else {
+    B[gwl] = tail;
   }
-  const uint32_t ni = gwl - gw0 - 1;
+  const uint32_t ni = gwl - gw0 - 1u;
   if (ni <= WT_WG_INLANE) {
-    for (uint32_t w = 0; w < ni; w++) B[gw0 + 1 + w] = lb_bits(LBw, ls + hb + 64u * w, 64);
+    for (uint32_t w = 0; w < ni; w++) B[gw0 + 1u + w] = lb_bits(LBw, ls + hb + 64u * w, 64);
     return 0u;
   }
   return ni;
@@ -343,6 +360,21 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(sz) : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(a0), "r"(sz), "r"(bar)
+               : "memory");
+}
+// lane 0: as bulk_load, plus a second 16-byte-aligned copy (bytes2 % 16 == 0) on the same barrier
+__device__ __forceinline__ void bulk_load2(uint32_t dst, const void *src, uint32_t bytes, uint32_t dst2,
+                                           const void *src2, uint32_t bytes2, uint32_t bar) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + bytes + 15) & ~(uintptr_t)15;
+  const uint32_t sz = (uint32_t)(a1 - a0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(sz + bytes2) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(a0), "r"(sz), "r"(bar)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst2),
+               "l"(src2), "r"(bytes2), "r"(bar)
                : "memory");
 }
 __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t phase) {
@@ -401,14 +433,15 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
   const uint32_t ndig = 1u << tau, dmask = ndig - 1u;
   const uint32_t pmask = pbits >= 32 ? 0xffffffffu : (1u << pbits) - 1u;
   const uint32_t nchains = p.counts[0];
+  const uint32_t n32 = (uint32_t)p.n;  // n < 2^32 (wt_build's contract)
   const InT *keys = reinterpret_cast<const InT *>(p.keys_in);
-  const uint32_t bar = smem_u32(&s.bar), stg = smem_u32(s.stage);
-  // thread 0: claim a chain and start the bulk copy of its first tile
+  const uint32_t bar = smem_u32(&s.bar), stg = smem_u32(s.stage), vA = smem_u32(s.V);
+  // thread 0: claim a chain and start the bulk copy of its first tile and its digit vector
   auto claim = [&]() {
     const uint32_t c = atomicAdd(p.chain_counter, 1u);
     if (c < nchains) {
       const uint32_t b = p.chain_begin[c], e = p.chain_end[c];
-      bulk_load(stg, keys + b, min(e - b, T) * IB, bar);
+      bulk_load2(stg, keys + b, min(e - b, T) * IB, vA, p.V + (uint64_t)c * 256, 1024u, bar);
     }
     return c;
   };
@@ -427,15 +460,15 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
     const uint32_t rstart = p.row_start[row];
     const uint32_t *Cg = p.Cseg + (uint64_t)row * (ndig + 1);
     uint32_t *X = reinterpret_cast<uint32_t *>(s.CW);  // scratch until the carries start
+    bar_wait(bar, phase);  // the chain's digit vector (and first tile) have landed
     if (warp == 0) {
-      const uint32_t cfirst = p.row_first[row];
       // X[d] = exclusive scan over digits of the same-row elements ahead of the chain
       uint32_t v[8], sum = 0;
       const uint32_t per = (ndig + 31) >> 5, lo = min(lane * per, ndig), hi = min(lo + per, ndig);
 #pragma unroll
       for (int i = 0; i < 8; i++) {
         const uint32_t d = lo + i;
-        v[i] = (d < hi) ? p.E[(uint64_t)d * p.estride + c] - p.E[(uint64_t)d * p.estride + cfirst] : 0u;
+        v[i] = (d < hi) ? s.V[d] : 0u;
         sum += v[i];
       }
       const uint32_t incl = warp_incl_scan(sum, lane);
@@ -468,8 +501,10 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
       const uint32_t nsc = (len + SC - 1) / SC, ntot = nsc * SC;
       const uint32_t c0 = min((uint32_t)warp * SPW, nsc), c1 = min(c0 + SPW, nsc);  // this warp's quarter
 
-      // ---- 1. records (bit-reversed keys) from the staged input + ones of bit 0 per quarter ----
-      bar_wait(bar, phase);
+      // ---- 1. records from the staged input + ones of bit 0 per quarter ----
+      // record = (payload << tau) | reversed digit: level l0+k's bit (the (k+1)'st highest
+      // bit of the key) is record bit k; the payload keeps its natural order
+      if (start64 != cbeg) bar_wait(bar, phase);
       phase ^= 1u;
       {
         const uint32_t h = (uint32_t)(reinterpret_cast<uintptr_t>(keys + start) & 15u);
@@ -486,12 +521,13 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
               if (kb < 8) x = (x >> (8u - kb)) & (((1u << kb) - 1u) * 0x01010101u);
               w[q] = x;
             }
-          } else if constexpr (IB == 4 && RB == 2) {
+          } else if (IB == 4 && RB == 2 && kb == 16 && tau == 8) {
+            // key = digit << 8 | payload (< 2^16): record bytes {rev8(digit), payload}
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-              uint32_t x = __byte_perm(__brev(in[2 * q]), __brev(in[2 * q + 1]), 0x7632);
-              if (kb < 16) x = (x >> (16u - kb)) & (((1u << kb) - 1u) * 0x00010001u);
-              w[q] = x;
+              const uint32_t r0 = __byte_perm(__brev(in[2 * q]), in[2 * q], 0x0042);
+              const uint32_t r1 = __byte_perm(__brev(in[2 * q + 1]), in[2 * q + 1], 0x0042);
+              w[q] = __byte_perm(r0, r1, 0x5410);
             }
           } else {
 #pragma unroll
@@ -502,7 +538,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
               if constexpr (IB == 1) key = (in[e >> 2] >> (8 * (e & 3))) & 0xffu;
               else if constexpr (IB == 2) key = (in[e >> 1] >> (16 * (e & 1))) & 0xffffu;
               else key = in[e];
-              w[(e * RB) >> 2] |= (__brev(key) >> (32u - kb)) << (8u * ((e * RB) & 3u));
+              const uint32_t r = ((__brev(key) >> (32u - kb)) & dmask) | ((key & pmask) << tau);
+              w[(e * RB) >> 2] |= r << (8u * ((e * RB) & 3u));
             }
           }
           if (i0 + PER > len) {  // padding records (all ones: a one at every level, they stay last)
@@ -602,18 +639,23 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
 #else
       for (uint32_t s0 = 1; s0 < ndig; s0 += NT) {
 #endif
-        const uint32_t slot = s0 + tid;
-        uint32_t ni = 0, gwA = 0, lsA = 0, kk = 0;
+        const uint32_t slot = s0 + lane * CT_WARPS + warp;  // interleaved: long runs spread over the warps
+        uint32_t ni = 0, gwA = 0, lsA = 0, kk = 0, Gr = 0, lsr = 0, cnr = 0;
         if (slot < ndig) {
           const uint32_t cn = s.C[slot];
           if (cn) {
             kk = 31 - __clz(slot);
             const uint32_t G = s.pos[slot], ls = s.S[slot];
             uint64_t *B = p.bits + (uint64_t)(p.l0 + kk) * p.wpl;
-            ni = wg_run(s.CW[slot], s.CF[slot], reinterpret_cast<const uint32_t *>(s.LB[kk]), B, p.n, G, ls, cn);
+            ni = wg_run(s.CW[slot], s.CF[slot], reinterpret_cast<const uint32_t *>(s.LB[kk]), B, n32, G, ls, cn);
             gwA = (G >> 6) + 1;
             lsA = ls + min(cn, 64u - (G & 63u));
             s.pos[slot] = G + cn;
+            Gr = G; lsr = ls; cnr = cn;
+            // fused A7: short runs count their blocks here, long ones below (lane per block)
+            if ((((G + cn - 1u) >> 9) - (G >> 9)) < 4u)
+              run_blocks(p.blkcnt + (uint64_t)(p.l0 + kk) * p.bpl, reinterpret_cast<const uint32_t *>(s.LB[kk]),
+                         s.RP[kk], G, ls, cn, G >> 9, (G + cn - 1u) >> 9, 1u);
           }
         }
         uint32_t m = __ballot_sync(FULL, ni != 0);
@@ -625,6 +667,15 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
           uint64_t *B = p.bits + (uint64_t)(p.l0 + k2) * p.wpl;
           const uint32_t *LBw = reinterpret_cast<const uint32_t *>(s.LB[k2]);
           for (uint32_t w = lane; w < nn; w += 32) B[g + w] = lb_bits(LBw, l0 + 64u * w, 64);
+        }
+        m = __ballot_sync(FULL, cnr != 0 && (((Gr + cnr - 1u) >> 9) - (Gr >> 9)) >= 4u);
+        while (m) {
+          const int src_l = __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t G = __shfl_sync(FULL, Gr, src_l), ls = __shfl_sync(FULL, lsr, src_l),
+                         cn = __shfl_sync(FULL, cnr, src_l), k2 = __shfl_sync(FULL, kk, src_l);
+          run_blocks(p.blkcnt + (uint64_t)(p.l0 + k2) * p.bpl, reinterpret_cast<const uint32_t *>(s.LB[k2]), s.RP[k2],
+                     G, ls, cn, (G >> 9) + lane, (G + cn - 1u) >> 9, 32u);
         }
       }
 
@@ -648,8 +699,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
 #pragma unroll 4
         for (uint32_t i = tid; i < len; i += NT) {
           const uint32_t r = R[i];
-          const uint32_t key = __brev(r) >> (32u - kb);
-          ko[KB[r & dmask] + i] = (OutT)(key & pmask);
+          ko[KB[r & dmask] + i] = (OutT)(r >> tau);
         }
       }
       __syncthreads();
@@ -657,8 +707,9 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
     // ---- chain end: flush carried words (shared with the next chain or row) ----
     for (uint32_t slot = 1 + tid; slot < ndig; slot += NT) {
       if (s.CF[slot] & CF_VALID) {
-        uint64_t *B = p.bits + (uint64_t)(p.l0 + (31 - __clz(slot))) * p.wpl;
-        atomicOr(reinterpret_cast<unsigned long long *>(&B[s.pos[slot] >> 6]), s.CW[slot]);
+        const uint32_t l = p.l0 + (31 - __clz(slot)), gw = s.pos[slot] >> 6;
+        uint64_t *B = p.bits + (uint64_t)l * p.wpl;
+        atomicOr(reinterpret_cast<unsigned long long *>(&B[gw]), s.CW[slot]);
       }
     }
     __syncthreads();
