@@ -507,12 +507,15 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     k_row_scan<<<(unsigned)((gb.max_rows * 32 + 255) / 256), 256, 0, s>>>(gb.E, stride, gb.row_first, gb.counts,
                                                                           gb.ndig, gb.Cseg, err);
     chk(cudaGetLastError());
-    if (gb.V)
+    rec.end();
+    if (gb.V) {
+      rec.begin("k_chain_vec", gb.max_chains * 256 * 12);
       k_chain_vec<<<(unsigned)((gb.max_chains * 32 + 255) / 256), 256, 0, s>>>(gb.E, stride, gb.chain_row,
                                                                               gb.row_first, gb.counts, gb.ndig, gb.V,
                                                                               err);
-    chk(cudaGetLastError());
-    rec.end();
+      chk(cudaGetLastError());
+      rec.end();
+    }
     // ---- A4: node table of this group's levels l0+k_lo .. l0+k_lo+nk-1 ----
     if (gb.nk && g == 0) {
       rec.begin("k_nodes_count", 0);
