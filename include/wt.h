@@ -106,8 +106,10 @@ int wt_build_host(const void *h_seq, uint64_t n, uint32_t elem_bytes, uint64_t s
                   void *stream, wt_tree **out);
 
 /* wt_free -- release everything owned by t: stream-ordered frees on the
- * build's stream (after any work queued there, e.g. queries).  NULL is a
- * no-op.  Returns WT_OK or WT_ECUDA. */
+ * build stream, after the work already enqueued on it and on every stream that
+ * a query (wt_access / wt_rank / wt_select) or wt_select_index of this tree
+ * used (the build stream waits for an event recorded on each).  Does not
+ * synchronise the host.  NULL is a no-op.  Returns WT_ECUDA if a free failed. */
 int wt_free(wt_tree *t);
 
 /*
@@ -161,7 +163,8 @@ typedef struct wm_matrix {
  * WT_EINVAL for bad arguments, one stream synchronisation at the end). */
 int wm_build(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma,
              void *stream, wm_matrix **out);
-/* wm_free -- release everything owned by m; NULL is a no-op. */
+/* wm_free -- release everything owned by m; NULL is a no-op.  Ordered like
+ * wt_free (after the build stream and every stream a query of m used). */
 int wm_free(wm_matrix *m);
 /* wm_access / wm_rank -- batched access(S, i) and inclusive rank_c(S, i)
  * on the matrix: a 0 bit at level l maps i to rank0(i),
@@ -256,7 +259,8 @@ typedef struct hwt_tree {
  * nothing leaks. */
 int hwt_build(const void *d_seq, uint64_t n, uint32_t elem_bytes, uint64_t sigma,
               void *stream, hwt_tree **out);
-/* hwt_free -- release everything owned by t; NULL is a no-op. */
+/* hwt_free -- release everything owned by t; NULL is a no-op.  Ordered like
+ * wt_free (after the build stream and every stream a query of t used). */
 int hwt_free(hwt_tree *t);
 /* hwt_access / hwt_rank -- batched access(S, i) and inclusive rank_c(S, i)
  * by descent along the code; rank_c of an absent symbol

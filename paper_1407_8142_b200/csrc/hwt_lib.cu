@@ -14,6 +14,7 @@ namespace {
 struct HwtInternal {
   cudaStream_t stream;
   std::vector<void *> outputs;
+  TouchSet touched;
   uint32_t *sym_sorted = nullptr;
   HuffCanon *canon = nullptr;
 };
@@ -30,8 +31,8 @@ void launch_sym_hist(const void *S, uint64_t n, uint32_t sigma, uint32_t *hist, 
     const unsigned grid = (unsigned)std::min<uint64_t>((n + 8191) / 8192, 4ull * num_sms());
     k_sym_hist_small<InT><<<grid, 512, 0, s>>>((const InT *)S, n, sigma, hist, err);
   } else {
-    static std::once_flag f;
-    std::call_once(f, [] {
+    static PerDevice<int> attr;
+    attr.get([](int &) {
       cudaFuncSetAttribute(k_sym_hist<InT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_PART * 4);
     });
     const uint32_t nparts = (sigma + HIST_PART - 1) / HIST_PART;
@@ -46,8 +47,8 @@ void launch_map_t(const void *S, uint64_t n, uint32_t sigma, const uint32_t *pad
   const size_t tab = (size_t)sigma * sizeof(OutT);
   const unsigned grid = (unsigned)std::min<uint64_t>((n + 2047) / 2048, 4ull * num_sms());
   if (tab <= 160 * 1024) {
-    static std::once_flag f;
-    std::call_once(f, [] {
+    static PerDevice<int> attr;
+    attr.get([](int &) {
       cudaFuncSetAttribute(k_huff_map<InT, OutT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     });
     k_huff_map<InT, OutT, true><<<grid, 512, tab, s>>>((const InT *)S, n, sigma, pad, (OutT *)X);
@@ -282,7 +283,7 @@ int hwt_build_impl(const void *d_seq, uint64_t n, uint32_t eb, uint64_t sigma, v
         chk(cudaGetLastError());
       }
       done.push_back(sg_);
-      const int frc = wt_free(pt);  // stream-ordered after the kernels above; synchronises
+      const int frc = wt_free(pt);  // stream-ordered after the kernels above (same stream)
       if (frc != WT_OK) return fail(WT_ECUDA);
     }
     for (uint32_t l = 0; l < h; l++) h_np[l + 1] += h_np[l];
@@ -364,23 +365,28 @@ int hwt_free(hwt_tree *t) {
   if (!t) return WT_OK;
   HwtInternal *in = static_cast<HwtInternal *>(t->internal);
   cudaError_t e = cudaSuccess;
-  if (in) {
+  if (in) {  // stream-ordered, after the build stream and every stream a query used (as wt_free)
+    e = in->touched.order_before(in->stream);
     for (void *p : in->outputs) {
       cudaError_t e2 = cudaFreeAsync(p, in->stream);
       if (e2 != cudaSuccess) e = e2;
     }
-    cudaError_t e3 = cudaStreamSynchronize(in->stream);
-    if (e3 != cudaSuccess) e = e3;
     delete in;
   }
   delete t;
   return e == cudaSuccess ? WT_OK : WT_ECUDA;
 }
 
+static void touch_hwt(const hwt_tree *t, void *stream) {
+  HwtInternal *in = static_cast<HwtInternal *>(t->internal);
+  in->touched.add(static_cast<cudaStream_t>(stream), in->stream);
+}
+
 int hwt_access(const hwt_tree *t, const uint64_t *d_pos, uint64_t q, uint32_t *d_out, void *stream) {
   if (!t || !t->internal || (q > 0 && (!d_pos || !d_out))) return WT_EINVAL;
   if (q == 0) return WT_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  touch_hwt(t, stream);
   k_hwt_access<<<(unsigned)((q + 255) / 256), 256, 0, s>>>(view_of_hwt(t), d_pos, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
 }
@@ -390,6 +396,7 @@ int hwt_rank(const hwt_tree *t, const uint32_t *d_sym, const uint64_t *d_pos, ui
   if (!t || !t->internal || (q > 0 && (!d_sym || !d_pos || !d_out))) return WT_EINVAL;
   if (q == 0) return WT_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  touch_hwt(t, stream);
   k_hwt_rank<<<(unsigned)((q + 255) / 256), 256, 0, s>>>(view_of_hwt(t), d_sym, d_pos, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
 }
@@ -399,6 +406,7 @@ int hwt_select(const hwt_tree *t, const uint32_t *d_sym, const uint64_t *d_k, ui
   if (!t || !t->internal || (q > 0 && (!d_sym || !d_k || !d_out))) return WT_EINVAL;
   if (q == 0) return WT_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  touch_hwt(t, stream);
   k_hwt_select<<<(unsigned)((q + 127) / 128), 128, 0, s>>>(view_of_hwt(t), d_sym, d_k, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
 }

@@ -21,9 +21,8 @@ struct WmLaunch {
 
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
 WmLaunch wm_launch() {
-  static WmLaunch wl;
-  static std::once_flag f;
-  std::call_once(f, [] {
+  static PerDevice<WmLaunch> pd_;
+  return pd_.get([](WmLaunch &wl) {
 #ifdef WT_WM_WARP  // the one-warp pass (kept for comparison)
     wl.kern = k_wm_group<InT, RecT, OutT, HAS_OUT>;
     wl.tile = WmTile<RecT>::TW;
@@ -37,7 +36,6 @@ WmLaunch wm_launch() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wl.kern, wl.block, 0);
     wl.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
   });
-  return wl;
 }
 
 WmLaunch pick_wm(uint32_t inw, uint32_t recw, uint32_t outw, bool has_out) {
@@ -60,6 +58,7 @@ WmLaunch pick_wm(uint32_t inw, uint32_t recw, uint32_t outw, bool has_out) {
 struct WmInternal {
   cudaStream_t stream;
   std::vector<void *> outputs;
+  TouchSet touched;
 };
 
 int wm_build_impl(const void *d_seq, uint64_t n, uint32_t eb, uint64_t sigma, void *stream_v, wm_matrix **out) {
@@ -120,6 +119,9 @@ int wm_build_impl(const void *d_seq, uint64_t n, uint32_t eb, uint64_t sigma, vo
     maxK = std::max(maxK, gr.K);
     gr.keys_out = g + 1 < NG ? A.alloc<uint8_t>(n * gr.outw, false) : nullptr;
   }
+  // sigma == 1 (no group): validation in chains of 2^24 symbols (32-bit chain arithmetic)
+  constexpr uint64_t VCH = 1ull << 24;
+  if (!NG) maxK = std::max<uint64_t>((n + VCH - 1) / VCH, 1);
   // chain tables (reused by every group: one row, the whole sequence)
   uint32_t *cb = A.alloc<uint32_t>(maxK, false), *ce_ = A.alloc<uint32_t>(maxK, false);
   uint32_t *cr = A.alloc<uint32_t>(maxK, false), *rf = A.alloc<uint32_t>(2, false);
@@ -144,11 +146,12 @@ int wm_build_impl(const void *d_seq, uint64_t n, uint32_t eb, uint64_t sigma, vo
   bool side_used = false;
   const void *keys_in = d_seq;
   if (n && !NG) {  // sigma == 1: validation only (every symbol must be 0)
-    const uint64_t CH = std::max<uint64_t>(n, 1);
-    k_chains_root<<<1, 256, 0, s>>>(n, CH, 1, cb, ce_, cr, rf, rs, rk, cnt, err);
-    if (eb == 1) k_chain_hist<uint8_t, true><<<1, 512, 0, s>>>((const uint8_t *)d_seq, sigma, 0, 1, cb, ce_, cnt, 2, E, err);
-    else if (eb == 2) k_chain_hist<uint16_t, true><<<1, 512, 0, s>>>((const uint16_t *)d_seq, sigma, 0, 1, cb, ce_, cnt, 2, E, err);
-    else k_chain_hist<uint32_t, true><<<1, 512, 0, s>>>((const uint32_t *)d_seq, sigma, 0, 1, cb, ce_, cnt, 2, E, err);
+    const uint32_t K = (uint32_t)maxK, st = K + 1;
+    const unsigned hg = std::min<uint32_t>(K, 4 * num_sms());
+    k_chains_root<<<(K + 255) / 256, 256, 0, s>>>(n, VCH, K, cb, ce_, cr, rf, rs, rk, cnt, err);
+    if (eb == 1) k_chain_hist<uint8_t, true><<<hg, 512, 0, s>>>((const uint8_t *)d_seq, sigma, 0, 1, cb, ce_, cnt, st, E, err);
+    else if (eb == 2) k_chain_hist<uint16_t, true><<<hg, 512, 0, s>>>((const uint16_t *)d_seq, sigma, 0, 1, cb, ce_, cnt, st, E, err);
+    else k_chain_hist<uint32_t, true><<<hg, 512, 0, s>>>((const uint32_t *)d_seq, sigma, 0, 1, cb, ce_, cnt, st, E, err);
     chk(cudaGetLastError());
   }
   for (uint32_t g = 0; g < NG && n; g++) {
@@ -258,17 +261,23 @@ int wm_free(wm_matrix *m) {
   if (!m) return WT_OK;
   WmInternal *in = static_cast<WmInternal *>(m->internal);
   cudaError_t e = cudaSuccess;
-  if (in) {
+  if (in) {  // stream-ordered, after the build stream and every stream a query used (as wt_free)
+    e = in->touched.order_before(in->stream);
     for (void *p : in->outputs) {
       const cudaError_t e2 = cudaFreeAsync(p, in->stream);
       if (e2 != cudaSuccess) e = e2;
     }
-    const cudaError_t e3 = cudaStreamSynchronize(in->stream);
-    if (e3 != cudaSuccess) e = e3;
     delete in;
   }
   delete m;
   return e == cudaSuccess ? WT_OK : WT_ECUDA;
+}
+
+static void touch_wm(const wm_matrix *m, void *stream) {
+  if (m && m->internal) {
+    WmInternal *in = static_cast<WmInternal *>(m->internal);
+    in->touched.add(static_cast<cudaStream_t>(stream), in->stream);
+  }
 }
 
 static TreeView view_of_wm(const wm_matrix *m) {
@@ -287,6 +296,7 @@ static TreeView view_of_wm(const wm_matrix *m) {
 int wm_access(const wm_matrix *m, const uint64_t *d_pos, uint64_t q, uint32_t *d_out, void *stream) {
   if (!m || (q > 0 && (!d_pos || !d_out))) return WT_EINVAL;
   if (q == 0) return WT_OK;
+  touch_wm(m, stream);
   k_wm_access<<<(unsigned)((q + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(view_of_wm(m), m->zeros,
                                                                                            d_pos, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
@@ -295,6 +305,7 @@ int wm_access(const wm_matrix *m, const uint64_t *d_pos, uint64_t q, uint32_t *d
 int wm_select_index(wm_matrix *m, void *stream) {
   if (!m || !m->internal) return WT_EINVAL;
   WmInternal *in = static_cast<WmInternal *>(m->internal);
+  touch_wm(m, stream);
   return select_index_impl(view_of_wm(m), &m->select_per_level, &m->select0, &m->select1, in->outputs,
                            static_cast<cudaStream_t>(stream));
 }
@@ -303,6 +314,7 @@ int wm_select(const wm_matrix *m, const uint32_t *d_sym, const uint64_t *d_k, ui
               void *stream) {
   if (!m || (q > 0 && (!d_sym || !d_k || !d_out)) || !m->select_per_level) return WT_EINVAL;
   if (q == 0) return WT_OK;
+  touch_wm(m, stream);
   k_wm_select<<<(unsigned)((q + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       view_of_wm(m), m->zeros, m->select0, m->select1, m->select_per_level, m->sigma, d_sym, d_k, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
@@ -312,6 +324,7 @@ int wm_rank(const wm_matrix *m, const uint32_t *d_sym, const uint64_t *d_pos, ui
             void *stream) {
   if (!m || (q > 0 && (!d_sym || !d_pos || !d_out))) return WT_EINVAL;
   if (q == 0) return WT_OK;
+  touch_wm(m, stream);
   k_wm_rank<<<(unsigned)((q + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       view_of_wm(m), m->zeros, m->sigma, d_sym, d_pos, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;

@@ -128,9 +128,37 @@ struct Recorder {
   }
 };
 
+// Streams other than the build stream on which queries / select indexes of a
+// structure were enqueued: its free waits for them (an event per stream)
+// before releasing the memory on the build stream.
+struct TouchSet {
+  std::mutex mu;
+  std::vector<cudaStream_t> streams;
+  void add(cudaStream_t s, cudaStream_t build) {
+    if (s == build) return;
+    std::lock_guard<std::mutex> g(mu);
+    for (cudaStream_t x : streams)
+      if (x == s) return;
+    streams.push_back(s);
+  }
+  cudaError_t order_before(cudaStream_t build) {  // build stream waits for every touched stream
+    std::lock_guard<std::mutex> g(mu);
+    cudaError_t e = cudaSuccess;
+    for (cudaStream_t x : streams) {
+      cudaEvent_t ev;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return cudaErrorUnknown;
+      if (cudaEventRecord(ev, x) != cudaSuccess || cudaStreamWaitEvent(build, ev, 0) != cudaSuccess)
+        e = cudaErrorUnknown;
+      cudaEventDestroy(ev);
+    }
+    return e;
+  }
+};
+
 struct Internal {
   cudaStream_t stream;
   std::vector<void *> outputs;
+  TouchSet touched;
 };
 
 inline uint32_t levels_of(uint64_t sigma) {
@@ -140,33 +168,47 @@ inline uint32_t levels_of(uint64_t sigma) {
   return L;
 }
 
+// Per-device lazily initialised state: a process may drive several GPUs, so
+// launch configurations, function attributes, side streams and pool settings
+// are kept per device (the current device of the calling thread).
+constexpr int MAX_DEV = 64;
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d < 0 || d >= MAX_DEV) ? 0 : d;
+}
+template <typename T>
+struct PerDevice {
+  T v[MAX_DEV]{};
+  std::once_flag f[MAX_DEV];
+  template <typename Init>
+  T &get(Init init) {
+    const int d = cur_device();
+    std::call_once(f[d], [&] { init(v[d]); });
+    return v[d];
+  }
+};
+
 // A second stream of the same device for the rank directory of finished
-// level groups, so that it overlaps the next group pass (created once).
+// level groups, so that it overlaps the next group pass (created once per device).
 inline cudaStream_t side_stream() {
-  static cudaStream_t side = nullptr;
-  static std::once_flag f;
-  std::call_once(f, [] { cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking); });
-  return side;
+  static PerDevice<cudaStream_t> side;
+  return side.get([](cudaStream_t &st) { cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking); });
 }
 
-inline int g_num_sms = 0;
 inline int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
+  static PerDevice<int> sms;
+  return sms.get([](int &v) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, cur_device());
+    if (v <= 0) v = 148;
+  });
 }
 
 inline void configure_pool_once() {
-  static std::once_flag f;
-  std::call_once(f, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static PerDevice<int> done;
+  done.get([](int &) {
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (cudaDeviceGetDefaultMemPool(&pool, cur_device()) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
@@ -183,9 +225,9 @@ struct Arena {
   size_t cap = 0, used = 0, want = 0;
   bool busy = false;
 };
-inline Arena &thread_arena() {
-  static thread_local Arena a;
-  return a;
+inline Arena &thread_arena() {  // per host thread and device (the arena's memory lives on that device)
+  static thread_local Arena a[MAX_DEV];
+  return a[cur_device()];
 }
 constexpr size_t ARENA_MAX = 64ull << 20;
 

@@ -33,9 +33,8 @@ struct GroupLaunch {
 
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
 GroupLaunch group_launch() {
-  static GroupLaunch gl;
-  static std::once_flag f;
-  std::call_once(f, [] {
+  static PerDevice<GroupLaunch> pd_;
+  return pd_.get([](GroupLaunch &gl) {
     gl.kern = k_group<InT, RecT, OutT, HAS_OUT>;
     gl.smem = 0;  // static shared memory
     gl.tile = GroupTile<RecT>::TT;
@@ -45,15 +44,13 @@ GroupLaunch group_launch() {
     gl.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
     gl.workers = gl.grid;
   });
-  return gl;
 }
 
 // k_wgroup: one chain per CTA at a time, dynamic shared memory
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
 GroupLaunch wgroup_launch() {
-  static GroupLaunch gl;
-  static std::once_flag f;
-  std::call_once(f, [] {
+  static PerDevice<GroupLaunch> pd_;
+  return pd_.get([](GroupLaunch &gl) {
     gl.kern = k_wgroup<InT, RecT, OutT, HAS_OUT>;
     gl.smem = sizeof(WGSmem<InT, RecT, HAS_OUT>);
     gl.tile = WGTile<RecT>::T;
@@ -64,7 +61,6 @@ GroupLaunch wgroup_launch() {
     gl.grid = num_sms() * (per_sm < 1 ? 1 : per_sm);
     gl.workers = gl.grid;  // one chain per CTA at a time
   });
-  return gl;
 }
 
 inline bool use_old_group() {
@@ -87,9 +83,8 @@ struct LocalLaunch {
 
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
 LocalLaunch local_launch() {
-  static LocalLaunch ll;
-  static std::once_flag f;
-  std::call_once(f, [] {
+  static PerDevice<LocalLaunch> pd_;
+  return pd_.get([](LocalLaunch &ll) {
     ll.count = k_local<InT, RecT, OutT, HAS_OUT, LM_COUNT>;
     ll.build = k_local<InT, RecT, OutT, HAS_OUT, LM_BUILD>;
     ll.big = k_local<InT, RecT, OutT, HAS_OUT, LM_BIG>;
@@ -106,7 +101,6 @@ LocalLaunch local_launch() {
     setup(ll.build, ll.smem, &ll.grid);
     setup(ll.big, ll.smem_big, &ll.grid_big);
   });
-  return ll;
 }
 
 LocalLaunch pick_local(uint32_t inw, uint32_t recw, uint32_t outw, bool has_out) {
@@ -379,7 +373,8 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   for (uint32_t g = 0; g < NG || (g == 0 && L == 0); g++) {
     // ---- chains of this group + their digit histograms (A1 for g = 0) ----
     if (g == 0) {
-      const uint64_t CH0 = NG ? G[0].CH : std::max<uint64_t>(n, 1);
+      // sigma == 1 (no group): validation in chains of 2^24 symbols (32-bit chain arithmetic)
+      const uint64_t CH0 = NG ? G[0].CH : (1ull << 24);
       const uint32_t K = NG ? (uint32_t)G[0].max_chains : (uint32_t)((n + CH0 - 1) / CH0);
       const uint32_t tau0 = NG ? G[0].tau : 0;
       const uint32_t ndig0 = 1u << tau0;
@@ -463,7 +458,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       const bool has_out = g + 1 < NG;
       char name[32];
       snprintf(name, sizeof(name), "k_group%u", g);
-      rec.begin(name, n * gb.inw + (has_out ? n * gb.outw : 0) + (uint64_t)gb.tau * n / 8);
+      rec.begin(name, (uint64_t)gb.tau * WPL * 8);  // algorithmic: the group's bitmap levels
       gb.ll.build<<<gb.ll.grid, LOCAL_WARPS * 32, gb.ll.smem, s>>>(lp);
       chk(cudaGetLastError());
       chk(cudaMemsetAsync(gb.bcounts, 0, sizeof(uint32_t), s));  // claim counter for the deferred rows
@@ -570,7 +565,9 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     const bool has_out = g + 1 < NG;
     char name[32];
     snprintf(name, sizeof(name), "k_group%u", g);
-    rec.begin(name, n * gb.inw + (has_out ? n * gb.outw : 0) + (uint64_t)gb.tau * n / 8);
+    // algorithmic bytes: S read once (group 0) + the group's bitmap
+    // levels; the narrowed keys between groups are overhead, not counted
+    rec.begin(name, (g == 0 ? n * eb : 0) + (uint64_t)gb.tau * WPL * 8);
     gb.gl.kern<<<gb.gl.grid, gb.gl.threads, gb.gl.smem, s>>>(gp);
     chk(cudaGetLastError());
     rec.end();
@@ -657,7 +654,10 @@ int wt_free(wt_tree *t) {
   Internal *in = static_cast<Internal *>(t->internal);
   cudaError_t e = cudaSuccess;
   if (in) {
-    for (void *p : in->outputs) {  // stream-ordered: after the work queued on the build stream
+    // stream-ordered: after the work queued on the build stream and on every
+    // stream a query or select index of this tree used
+    e = in->touched.order_before(in->stream);
+    for (void *p : in->outputs) {
       cudaError_t e2 = cudaFreeAsync(p, in->stream);
       if (e2 != cudaSuccess) e = e2;
     }
@@ -665,6 +665,13 @@ int wt_free(wt_tree *t) {
   }
   delete t;
   return e == cudaSuccess ? WT_OK : WT_ECUDA;
+}
+
+static void touch(const wt_tree *t, void *stream) {
+  if (t && t->internal) {
+    Internal *in = static_cast<Internal *>(t->internal);
+    in->touched.add(static_cast<cudaStream_t>(stream), in->stream);
+  }
 }
 
 static TreeView view_of(const wt_tree *t) {
@@ -684,6 +691,7 @@ int wt_access(const wt_tree *t, const uint64_t *d_pos, uint64_t q, uint32_t *d_o
   if (!t || (q > 0 && (!d_pos || !d_out))) return WT_EINVAL;
   if (q == 0) return WT_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  touch(t, stream);
   k_access<<<(unsigned)((q + 255) / 256), 256, 0, s>>>(view_of(t), d_pos, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
 }
@@ -693,6 +701,7 @@ int wt_rank(const wt_tree *t, const uint32_t *d_sym, const uint64_t *d_pos, uint
   if (!t || (q > 0 && (!d_sym || !d_pos || !d_out))) return WT_EINVAL;
   if (q == 0) return WT_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  touch(t, stream);
   k_rank_query<<<(unsigned)((q + 255) / 256), 256, 0, s>>>(view_of(t), t->sigma, d_sym, d_pos, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;
 }
@@ -759,6 +768,7 @@ extern "C" {
 int wt_select_index(wt_tree *t, void *stream) {
   if (!t || !t->internal) return WT_EINVAL;
   Internal *in = static_cast<Internal *>(t->internal);
+  touch(t, stream);
   return select_index_impl(view_of(t), &t->select_per_level, &t->select0, &t->select1, in->outputs,
                            static_cast<cudaStream_t>(stream));
 }
@@ -767,6 +777,7 @@ int wt_select(const wt_tree *t, const uint32_t *d_sym, const uint64_t *d_k, uint
               void *stream) {
   if (!t || (q > 0 && (!d_sym || !d_k || !d_out)) || !t->select_per_level) return WT_EINVAL;
   if (q == 0) return WT_OK;
+  touch(t, stream);
   k_wt_select<<<(unsigned)((q + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       view_of(t), t->select0, t->select1, t->select_per_level, t->sigma, d_sym, d_k, q, d_out);
   return cudaGetLastError() == cudaSuccess ? WT_OK : WT_ECUDA;

@@ -128,14 +128,14 @@ __global__ void __launch_bounds__(512) k_chain_hist(const T *__restrict__ keys, 
   const int head = (int)((sb - ab) / sizeof(T));
   const uint4 *V = reinterpret_cast<const uint4 *>(ab);
   const uint32_t len = end - beg;
-  const uint32_t nv = (head + len + PER - 1) / PER;
+  const uint32_t nv = (uint32_t)(((uint64_t)head + len + PER - 1) / PER);
   for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
     const uint4 q = __ldcs(V + i);
     const T *e = reinterpret_cast<const T *>(&q);
 #pragma unroll
     for (int k = 0; k < PER; k++) {
-      const int pos = (int)(i * PER + k) - head;
-      if (pos >= 0 && pos < (int)len) add((uint32_t)e[k]);
+      const int64_t pos = (int64_t)i * PER + k - head;
+      if (pos >= 0 && pos < (int64_t)len) add((uint32_t)e[k]);
     }
   }
   __syncthreads();

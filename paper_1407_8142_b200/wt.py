@@ -131,18 +131,23 @@ def _load():
 
 
 class _CAI:
-    """Minimal __cuda_array_interface__ wrapper for a library-owned array."""
+    """Minimal __cuda_array_interface__ wrapper for a library-owned array.  It
+    holds a reference to the owning structure, and torch keeps this object alive
+    as long as the tensor view: a view keeps its tree (matrix) from being
+    garbage-collected.  An explicit free() still releases the memory and
+    invalidates every view (documented on free())."""
 
-    def __init__(self, ptr: int, count: int, typestr: str):
+    def __init__(self, ptr: int, count: int, typestr: str, owner=None):
+        self._owner = owner
         self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
                                          "data": (int(ptr or 0), False), "version": 3,
                                          "strides": None}
 
 
-def _view(ptr, count, typestr, dtype, device):
+def _view(ptr, count, typestr, dtype, device, owner=None):
     if count == 0 or not ptr:
         return torch.zeros(0, dtype=dtype, device=device)
-    return torch.as_tensor(_CAI(ptr, count, typestr), device=device)
+    return torch.as_tensor(_CAI(ptr, count, typestr, owner), device=device)
 
 
 def _stream_ptr(stream) -> int:
@@ -165,8 +170,8 @@ class _SelectOps:
         sps = int(h.select_per_level)
         cnt = self.levels * sps
         return {"select_per_level": sps,
-                "select0": _view(h.select0, cnt, "<u4", torch.uint32, self.device),
-                "select1": _view(h.select1, cnt, "<u4", torch.uint32, self.device)}
+                "select0": _view(h.select0, cnt, "<u4", torch.uint32, self.device, self),
+                "select1": _view(h.select1, cnt, "<u4", torch.uint32, self.device, self)}
 
     def select(self, sym: torch.Tensor, k: torch.Tensor, stream=None) -> torch.Tensor:
         lib = _load()
@@ -199,7 +204,8 @@ class _Lazy:
     def __get__(self, obj, cls=None):
         if obj is None:
             return self
-        v = _view(getattr(obj.handle.contents, self.field), self.count(obj), self.typestr, self.dtype, obj.device)
+        v = _view(getattr(obj.handle.contents, self.field), self.count(obj), self.typestr, self.dtype, obj.device,
+                  obj)
         obj.__dict__[self.name] = v
         return v
 
@@ -248,6 +254,8 @@ class WaveletTree(_SelectOps):
         return rank(self, sym, pos, stream)
 
     def free(self):
+        """Release the tree (wt_free, stream-ordered).  Views of its arrays
+        taken earlier become invalid; views keep an unfreed tree alive."""
         if self._h is not None:
             for k in ("bits", "level_node_ptr", "node_key", "node_start", "rank_block", "rank_super"):
                 setattr(self, k, None)
@@ -379,10 +387,10 @@ class WaveletMatrix(_SelectOps):
         self.blocks_per_level = int(m.blocks_per_level)
         self.supers_per_level = int(m.supers_per_level)
         L = self.levels
-        self.bits = _view(m.bits, L * self.words_per_level, "<u8", torch.uint64, device)
-        self.zeros = _view(m.zeros, L, "<u8", torch.uint64, device)
-        self.rank_block = _view(m.rank_block, L * self.blocks_per_level, "<u2", torch.uint16, device)
-        self.rank_super = _view(m.rank_super, L * self.supers_per_level, "<u8", torch.uint64, device)
+        self.bits = _view(m.bits, L * self.words_per_level, "<u8", torch.uint64, device, self)
+        self.zeros = _view(m.zeros, L, "<u8", torch.uint64, device, self)
+        self.rank_block = _view(m.rank_block, L * self.blocks_per_level, "<u2", torch.uint16, device, self)
+        self.rank_super = _view(m.rank_super, L * self.supers_per_level, "<u8", torch.uint64, device, self)
 
     @property
     def handle(self):
@@ -506,7 +514,7 @@ class HuffmanWaveletTree:
         self.only_symbol = int(t.only_symbol)
         self.stages = int(t.stages)
         h = self.levels
-        u8 = lambda p, c: _view(p, c, "<u8", torch.uint64, device)  # noqa: E731
+        u8 = lambda p, c: _view(p, c, "<u8", torch.uint64, device, self)  # noqa: E731
         self.level_len = u8(t.level_len, h)
         self.level_word_ptr = u8(t.level_word_ptr, h + 1)
         self.level_block_ptr = u8(t.level_block_ptr, h + 1)
@@ -514,13 +522,13 @@ class HuffmanWaveletTree:
         wp, bp, sp = (int(x[-1]) if h else 0 for x in (self.level_word_ptr.cpu(), self.level_block_ptr.cpu(),
                                                         self.level_super_ptr.cpu()))
         self.bits = u8(t.bits, wp)
-        self.rank_block = _view(t.rank_block, bp, "<u2", torch.uint16, device)
+        self.rank_block = _view(t.rank_block, bp, "<u2", torch.uint16, device, self)
         self.rank_super = u8(t.rank_super, sp)
         self.level_node_ptr = u8(t.level_node_ptr, h + 1)
-        self.node_key = _view(t.node_key, self.total_nodes, "<u4", torch.uint32, device)
-        self.node_start = _view(t.node_start, self.total_nodes, "<u4", torch.uint32, device)
-        self.code = _view(t.code, self.sigma, "<u4", torch.uint32, device)
-        self.code_len = _view(t.code_len, self.sigma, "|u1", torch.uint8, device)
+        self.node_key = _view(t.node_key, self.total_nodes, "<u4", torch.uint32, device, self)
+        self.node_start = _view(t.node_start, self.total_nodes, "<u4", torch.uint32, device, self)
+        self.code = _view(t.code, self.sigma, "<u4", torch.uint32, device, self)
+        self.code_len = _view(t.code_len, self.sigma, "|u1", torch.uint8, device, self)
 
     @property
     def handle(self):

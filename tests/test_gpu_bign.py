@@ -144,3 +144,23 @@ def test_hwt_n_near_2_32():
         pre[c, 1:] = np.cumsum(P == c)
     assert np.array_equal(got.astype(np.int64), (pos >> 16) * cnt[sy] + pre[sy, (pos & 0xFFFF) + 1])
     t.free()
+
+
+def test_sigma1_validation_beyond_2_31():
+    """sigma = 1 (0 levels): validation alone; a nonzero symbol past position
+    2^31 must still give WT_ESYMBOL (tree and matrix)."""
+    import paper_1407_8142_b200 as wt
+    free, total = torch.cuda.mem_get_info()
+    if total < 32 << 30:
+        pytest.skip("needs a large-memory GPU")
+    n = (1 << 31) + 12345
+    S = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    t = wt.build(S, 1)
+    assert t.n == n and t.levels == 0
+    t.free()
+    S[(1 << 31) + 777] = 1
+    for build in (wt.build, wt.wm_build):
+        with pytest.raises(wt.WtError) as e:
+            build(S, 1)
+        assert e.value.code == -2  # WT_ESYMBOL
+    del S

@@ -94,8 +94,6 @@ def test_wm_unaligned_device_pointer(dtype, sigma):
 
 
 @pytest.mark.slow
-@pytest.mark.skipif(not __import__("os").environ.get("WT_LONG_TESTS"),
-                    reason="~4.5 min of oracle time; set WT_LONG_TESTS=1 (passed in round 1)")
 def test_wm_full_config5():
     """Config 5 (n = 2^29 u32, sigma = 2^32, 32 levels) at full size, every array."""
     cfg = gen.CONFIGS[5]
