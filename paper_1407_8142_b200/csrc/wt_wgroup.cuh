@@ -176,39 +176,41 @@ __device__ __forceinline__ void wg_split(uint8_t *LB, uint16_t *RP, uint32_t src
       Bz += SC - Sc;
     }
   } else if constexpr (RB == 2) {
+    // 16-bit records: the level bits are in the low (digit) bytes, so the 8
+    // digit bytes of the lane are gathered (2 PRMT) and the 8-bit SWAR above
+    // runs unchanged; addresses step 2 bytes per record (A.hi = 2)
     uint4 xn = lds128(sA + c0 * (SC * RB));
 #pragma unroll(WG_UNROLL)
     for (uint32_t c = c0; c < c1; c++) {
-      const uint32_t x[4] = {xn.x, xn.y, xn.z, xn.w};
+      const uint4 x = xn;
       if (c + 1 < c1) xn = lds128(sA + (c + 1) * (SC * RB));
-      uint32_t t[4], pre[4];
-#pragma unroll
-      for (int w = 0; w < 4; w++) t[w] = (x[w] >> k) & 0x00010001u;
-      uint32_t cin = 0, inc = 0;
-#pragma unroll
-      for (int w = 0; w < 4; w++) {  // exclusive prefix in 16-bit fields
-        pre[w] = (t[w] << 16) + cin;
-        inc = pre[w] + t[w];
-        cin = __byte_perm(inc, 0, 0x3232);
-      }
-      // high half of inc: ones of the lane (0..8)
-      const uint32_t O = __popc(ballot_m(inc, 1u << 16) & lt) + 2 * __popc(ballot_m(inc, 2u << 16) & lt) +
-                         4 * __popc(ballot_m(inc, 4u << 16) & lt) + 8 * __popc(ballot_m(inc, 8u << 16) & lt);
-      const uint32_t Sc = __shfl_sync(FULL, O + (inc >> 16), 31);
+      const uint32_t d_lo = __byte_perm(x.x, x.y, 0x6420), d_hi = __byte_perm(x.z, x.w, 0x6420);
+      const uint32_t t_lo = (d_lo >> k) & 0x01010101u, t_hi = (d_hi >> k) & 0x01010101u;
+      const uint32_t pre_lo = t_lo * 0x01010100u;
+      const uint32_t inc_lo = pre_lo + t_lo;
+      const uint32_t pre_hi = t_hi * 0x01010100u + __byte_perm(inc_lo, 0, 0x3333);
+      const uint32_t inc = pre_hi + t_hi;  // byte 3: ones of the lane (0..8)
+      const uint32_t O = __popc(ballot_m(inc, 1u << 24) & lt) + 2 * __popc(ballot_m(inc, 2u << 24) & lt) +
+                         4 * __popc(ballot_m(inc, 4u << 24) & lt) + 8 * __popc(ballot_m(inc, 8u << 24) & lt);
+      const uint32_t Sc = __shfl_sync(FULL, O + (inc >> 24), 31);
       if (!(lane & 3)) sts16(rpA + (c * 8u + (lane >> 2)) * 2u, SP + O);
-      const uint32_t u = t[0] | (t[1] << 2) | (t[2] << 4) | (t[3] << 6);
-      sts8(lbA + c * 32u + lane, u | (u >> 15));  // element j of the lane -> bit j
+      sts8(lbA + c * 32u + lane, (t_lo * 0x01020408u + t_hi * 0x10204080u) >> 24);
       if constexpr (MOVE) {
         const uint32_t D0 = Bz - 2u * O;
         const uint32_t A = (Bo + 2u * O - D0) | 0x20000u;
-#pragma unroll
-        for (int w = 0; w < 4; w++) {
-          const uint32_t M = t[w] * 0xffffu;
-          const uint32_t q = (pre[w] & M) | ((0x00010000u + 0x00020002u * w - pre[w]) & ~M);
-          const uint32_t tq = __byte_perm(t[w], q, 0x6240);
-          sts16(__dp2a_lo(A, tq, D0), x[w]);
-          sts16(__dp2a_hi(A, tq, D0), x[w] >> 16);
-        }
+        const uint32_t M_lo = t_lo * 0xffu, M_hi = t_hi * 0xffu;
+        const uint32_t q_lo = (pre_lo & M_lo) | ((0x03020100u - pre_lo) & ~M_lo);
+        const uint32_t q_hi = (pre_hi & M_hi) | ((0x07060504u - pre_hi) & ~M_hi);
+        const uint32_t tq0 = __byte_perm(t_lo, q_lo, 0x5140), tq1 = __byte_perm(t_lo, q_lo, 0x7362);
+        const uint32_t tq2 = __byte_perm(t_hi, q_hi, 0x5140), tq3 = __byte_perm(t_hi, q_hi, 0x7362);
+        sts16(__dp2a_lo(A, tq0, D0), x.x);
+        sts16(__dp2a_hi(A, tq0, D0), x.x >> 16);
+        sts16(__dp2a_lo(A, tq1, D0), x.y);
+        sts16(__dp2a_hi(A, tq1, D0), x.y >> 16);
+        sts16(__dp2a_lo(A, tq2, D0), x.z);
+        sts16(__dp2a_hi(A, tq2, D0), x.z >> 16);
+        sts16(__dp2a_lo(A, tq3, D0), x.w);
+        sts16(__dp2a_hi(A, tq3, D0), x.w >> 16);
       }
       SP += Sc;
       Bo += 2u * Sc;
@@ -253,15 +255,13 @@ __device__ __forceinline__ uint32_t wg_count(uint32_t src, uint32_t c0, uint32_t
       acc += ((x.x >> k) & 0x01010101u) + ((x.y >> k) & 0x01010101u);
     } else if constexpr (RB == 2) {
       const uint4 x = lds128(sA + c * (SC * RB));
-      acc += ((x.x >> k) & 0x00010001u) + ((x.y >> k) & 0x00010001u) + ((x.z >> k) & 0x00010001u) +
-             ((x.w >> k) & 0x00010001u);
+      acc += ((__byte_perm(x.x, x.y, 0x6420) >> k) & 0x01010101u) + ((__byte_perm(x.z, x.w, 0x6420) >> k) & 0x01010101u);
     } else {
       const uint2 x = lds64(sA + c * (SC * RB));
       acc += ((x.x >> k) & 1u) + ((x.y >> k) & 1u);
     }
   }
-  if constexpr (RB == 1) acc = (acc * 0x01010101u) >> 24;  // bytes <= 2 per superchunk: no overflow
-  else if constexpr (RB == 2) acc = (acc + (acc >> 16)) & 0xffffu;
+  if constexpr (RB <= 2) acc = (acc * 0x01010101u) >> 24;  // bytes <= 2 per superchunk: no overflow
   return __reduce_add_sync(FULL, acc);
 }
 
