@@ -158,6 +158,7 @@ __device__ __forceinline__ void wg_split(uint8_t *LB, uint16_t *RP, uint32_t src
       if constexpr (MOVE) {
         const uint32_t D0 = Bz - O;
         const uint32_t A = (Bo + O - D0) | 0x10000u;
+        WT_CHECK(D0 >= dst && Bo + O + 8u <= dst + nsc * SC * RB + 8u, 201);
         const uint32_t M_lo = t_lo * 0xffu, M_hi = t_hi * 0xffu;
         const uint32_t q_lo = (pre_lo & M_lo) | ((0x03020100u - pre_lo) & ~M_lo);
         const uint32_t q_hi = (pre_hi & M_hi) | ((0x07060504u - pre_hi) & ~M_hi);
@@ -198,6 +199,7 @@ __device__ __forceinline__ void wg_split(uint8_t *LB, uint16_t *RP, uint32_t src
       if constexpr (MOVE) {
         const uint32_t D0 = Bz - 2u * O;
         const uint32_t A = (Bo + 2u * O - D0) | 0x20000u;
+        WT_CHECK(D0 >= dst && Bo + 2u * O <= dst + nsc * SC * RB, 201);
         const uint32_t M_lo = t_lo * 0xffu, M_hi = t_hi * 0xffu;
         const uint32_t q_lo = (pre_lo & M_lo) | ((0x03020100u - pre_lo) & ~M_lo);
         const uint32_t q_hi = (pre_hi & M_hi) | ((0x07060504u - pre_hi) & ~M_hi);
@@ -305,6 +307,7 @@ __device__ __forceinline__ void run_blocks(uint32_t *bc, const uint32_t *LBw, co
   for (uint32_t b = b_lo; b <= b_hi; b += step) {
     const uint32_t lo = max(G, b << 9), hi = min(e, (b << 9) + 512u);
     const uint32_t c = wg_rank1(LBw, RP, ls + (hi - G)) - wg_rank1(LBw, RP, ls + (lo - G));
+    WT_CHECK(lo < hi && c <= hi - lo, 206);
     if (c) atomicAdd(bc + b, c);
   }
 }
@@ -312,6 +315,7 @@ __device__ __forceinline__ uint32_t wg_run(unsigned long long &cw, uint8_t &cf, 
                                            uint32_t n32, uint32_t G, uint32_t ls, uint32_t cnt) {
   const uint32_t g0 = G & 63u, e = G + cnt;
   const uint32_t gw0 = G >> 6, gwl = (e - 1u) >> 6;
+  WT_CHECK(cnt > 0 && (uint64_t)G + cnt <= n32, 203);
   const uint32_t hb = min(cnt, 64u - g0);
   uint64_t head = lb_bits(LBw, ls, hb) << g0;
   const uint32_t f = cf;
@@ -490,6 +494,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
       const uint32_t k = 31 - __clz(slot), r = slot - (1u << k);
       const uint32_t q = rev_bits(r, k), sh = tau - k;
       s.pos[slot] = rstart + Cg[q << sh] + (X[(q + 1) << sh] - X[q << sh]);
+      WT_CHECK(s.pos[slot] <= n32, 205);
     }
     __syncthreads();
     for (uint32_t i = tid; i < 256; i += NT) s.CF[i] = 0;
@@ -615,6 +620,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
         for (uint32_t r = tid; r < nk; r += NT) {
           const uint32_t st = s.S[nk + r], cn = s.C[nk + r];
           const uint32_t a = wg_rank1(LBw, s.RP[k], st), b = wg_rank1(LBw, s.RP[k], st + cn);
+          WT_CHECK(st + cn <= len && b >= a && b - a <= cn && a <= st, 202);
           s.C[2 * nk + r] = (uint16_t)(cn - (b - a));
           s.C[3 * nk + r] = (uint16_t)(b - a);
           s.S[2 * nk + r] = (uint16_t)(st - a);
@@ -632,6 +638,16 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
         classes_of(k);
         __syncthreads();
       }
+#ifdef WT_DEBUG
+      if (tid == 0) {
+        for (uint32_t k = 0; k <= kmax; k++) {
+          uint32_t sum = 0;
+          for (uint32_t r = 0; r < (1u << k); r++) sum += s.C[(1u << k) + r];
+          WT_CHECK(sum == len, 207);
+        }
+      }
+      __syncthreads();
+#endif
 
       // ---- 4. runs of every level (thread per class), long runs' interior words by the warp ----
 #ifdef WT_WG_DIAG_NORUNS
@@ -699,6 +715,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
 #pragma unroll 4
         for (uint32_t i = tid; i < len; i += NT) {
           const uint32_t r = R[i];
+          WT_CHECK((uint64_t)(uint32_t)(KB[r & dmask] + i) < p.n, 204);  // KB is a wrapped 32-bit base
           ko[KB[r & dmask] + i] = (OutT)(r >> tau);
         }
       }

@@ -8,11 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
-    "tb8k_w4": ["WT_CT_TB=8192", "WT_CT_WARPS=4"],
-    "tb16k_w4": ["WT_CT_TB=16384", "WT_CT_WARPS=4"],
-    "tb16k_w8": ["WT_CT_TB=16384", "WT_CT_WARPS=8"],
-    "tb8k_w8": ["WT_CT_TB=8192", "WT_CT_WARPS=8"],
-    "tb8k_w2": ["WT_CT_TB=8192", "WT_CT_WARPS=2"],
+    "debug": ["WT_DEBUG=1"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
