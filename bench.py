@@ -10,13 +10,16 @@ node table, all 16 levels of bitmaps with the fused splits, rank directory)
 plus wt_free.  Inputs (1 GiB) are larger than the 126 MB L2, so no explicit
 flush is needed between steps.
 
-Multi-GPU (torchrun): by default replicas -- each rank builds its own
-independent tree of the same configuration (seed + rank), value = all ranks'
-symbol-levels / max-over-ranks time, scaling "weak".  --sharded runs the
-sharded build instead (paper_1407_8142_b200/dist.py): the
-config's S split into N contiguous chunks, one per rank, one tree of S built
-cooperatively (digit all-gather, all-to-all over NCCL), complete on every
-rank; value = n*L / max-over-ranks time, scaling "strong".
+Multi-GPU (torchrun, N > 1): by default the sharded build
+(paper_1407_8142_b200/dist.py): the config's S
+split into N contiguous chunks, one per rank, one tree of S built
+cooperatively -- digit counts all-gathered, the MSD radix exchange over NCCL
+all-to-all, owners build the deep levels; the output stays distributed (each
+rank keeps its level slices; --gather also all-gathers the complete tree onto
+every rank); value = n*L / max-over-ranks time, scaling "strong".
+--replicas: each rank builds its own independent tree of the configuration
+(seed + rank), value = all ranks' symbol-levels / max-over-ranks time,
+scaling "weak".
 
 --impl reference times the CPU oracle (oracle/, single-threaded C, the
 paper's serialWT analogue) on a bounded sample of the same workload.
@@ -172,7 +175,9 @@ def main():
     ap.add_argument("--cpu-sample-log2", type=int, default=25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sharded", action="store_true", help="cooperative sharded build (strong scaling)")
+    ap.add_argument("--sharded", action="store_true", help="cooperative sharded build (default when N > 1)")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent trees per rank (weak scaling)")
+    ap.add_argument("--gather", action="store_true", help="sharded: all-gather the complete tree onto every rank")
     args = ap.parse_args()
 
     import gen
@@ -226,7 +231,7 @@ def main():
         if world > 1:
             dist.barrier()
 
-    if args.sharded:
+    if args.sharded or (world > 1 and not args.replicas):
         return bench_sharded(args, cfg, workload, rank, world, local_rank, dist, wt)
 
     # input: the config stream (rank r of a replica run uses seed + r)
@@ -345,19 +350,26 @@ def main():
 
 
 def bench_sharded(args, cfg, workload, rank, world, local_rank, dist, wt):
-    """--sharded: one tree of the config's S built by all ranks together."""
+    """One tree of the config's S built by all ranks together."""
     import torch
     from paper_1407_8142_b200 import dist as wdist
     S_host = gen_config(cfg)
     lo, hi = cfg.n * rank // world, cfg.n * (rank + 1) // world
-    S_dev = torch.from_numpy(S_host[lo:hi].copy()).cuda()
+    S_pin = torch.from_numpy(S_host[lo:hi].copy()).pin_memory()
+    S_dev = S_pin.cuda()
     del S_host
     comm = wdist.TorchComm() if world > 1 else _SoloComm()
+
+    def step(S):
+        t = wdist.build_sharded(S, cfg.sigma, comm, gather=args.gather)
+        t.free()
+
     for _ in range(args.warmup):
-        wdist.build_sharded(S_dev, cfg.sigma, comm).free()
+        step(S_dev)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     sampler = ClockSampler(local_rank)
+    wt.profile_enable(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -366,20 +378,40 @@ def bench_sharded(args, cfg, workload, rank, world, local_rank, dist, wt):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            wdist.build_sharded(S_dev, cfg.sigma, comm).free()
+            step(S_dev)
         e1.record(stream)
         torch.cuda.synchronize()
+    launches = wt.last_profile(total=True)["total_launches"]
+    wt.profile_enable(False)
     if world > 1:
         dist.barrier()
-    ms, value = aggregate(e0.elapsed_time(e1) / args.steps, cfg.n * cfg.levels // world, world,
+    units = cfg.n * cfg.levels  # one tree of the whole S (strong scaling)
+    ms, value = aggregate(e0.elapsed_time(e1) / args.steps, units // world, world,
                           dist if world > 1 else None, torch.device("cuda"))
+    # end to end: this rank's chunk copied from pinned host memory every step
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(S_pin.cuda(non_blocking=True))
+    t1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms, e2e_val = aggregate(t0.elapsed_time(t1) / args.steps, units // world, world,
+                                dist if world > 1 else None, torch.device("cuda"))
     if rank == 0:
-        workload = dict(workload, parallelism=f"shard{world}")
+        workload = dict(workload, parallelism=f"shard{world}", output="complete tree on every rank" if args.gather
+                        else "distributed (level slices per rank)")
+        tau = min(8, cfg.levels)
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32" if cfg.elem_bytes == 4 else "u8", "data": "synthetic",
-            "config": workload, "mode": "sharded", "clocks": sampler.summary(),
+            "config": workload, "mode": "sharded", "clocks": sampler.summary(), "gpu_launches": launches,
+            "e2e": {"value": e2e_val, "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": (hi - lo) * cfg.elem_bytes,
+                    "d2h_bytes_per_step": world * ((1 << tau) + 1) * 8},  # the all-gathered digit counts
             "gpu": torch.cuda.get_device_name(local_rank)}))
     if world > 1:
         dist.destroy_process_group()

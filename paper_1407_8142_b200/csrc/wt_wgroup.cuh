@@ -63,7 +63,11 @@ struct WGTile {
 #ifndef WT_CT_TB
 #define WT_CT_TB 8192
 #endif
-  static constexpr int T = WT_CT_TB / (int)sizeof(RecT);  // records per tile (WT_CT_TB bytes of records)
+#ifndef WT_CT_TB16
+#define WT_CT_TB16 6144
+#endif
+  // records per tile (WT_CT_TB bytes of records; WT_CT_TB16 for 16-bit records)
+  static constexpr int T = (sizeof(RecT) == 2 ? WT_CT_TB16 : WT_CT_TB) / (int)sizeof(RecT);
   static constexpr int SPW = T / SC / CT_WARPS;           // superchunks per warp
   static_assert(SPW >= 1 && T % (SC * CT_WARPS) == 0, "whole superchunks per warp");
 };

@@ -143,11 +143,59 @@ def plan_owners(D: np.ndarray, P: int) -> np.ndarray:
     return np.minimum(P - 1, (start * P) // n)
 
 
-def build_sharded(S_local: torch.Tensor, sigma: int, comm=None, ops=None):
+class ShardedPart:
+    """One rank's share of a sharded build (``build_sharded(..., gather=False)``),
+    before any bitmap crosses the interconnect:
+
+    * ``top``: the tree of this rank's chunk over the top ``tau`` digit bits;
+      its level k < tau run of class p is the global level-k run of class p
+      restricted to this rank, placed at ``C_k(p)`` + the earlier ranks' class-p
+      counts (``place_top`` gives those offsets);
+    * ``deep``: the owner's tree of the elements whose top digit it owns (a
+      contiguous digit range), in S_tau order; its level l >= tau is the
+      global level l on positions ``[R_o, R_o + n_o)``, its nodes the global
+      nodes of those levels with starts shifted by ``R_o``;
+    * ``C``: every rank's digit counts (rank x digit), ``owner``: the owner of
+      every digit.
+
+    Every global bitmap bit and node is held by exactly one rank; ``assemble``
+    (the all-gather of step 4) turns the parts into the complete tree."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+    def place_top(self, k: int) -> dict:
+        """{class p: (global offset of this rank's run, length)} of level k < tau."""
+        w = self.tau - k
+        out = {}
+        for p in range(1 << k):
+            lo_d, hi_d = p << w, (p + 1) << w
+            c = int(self.C[self.rank, lo_d:hi_d].sum())
+            if c:
+                out[p] = (int(self.dstart[lo_d]) + int(self.C[:self.rank, lo_d:hi_d].sum()), c)
+        return out
+
+    def free(self):
+        for t in (self.top, self.deep):
+            if t is not None and hasattr(t, "free"):
+                t.free()
+        self.top = self.deep = None
+
+
+def build_sharded(S_local: torch.Tensor, sigma: int, comm=None, ops=None, gather: bool = True):
     """Build the wavelet tree of S = concat over ranks of S_local (rank order).
 
-    Collective: every rank of ``comm`` must call it.  Returns the complete tree
-    on every rank (a ``WaveletTree`` with the CUDA ops)."""
+    Collective: every rank of ``comm`` must call it.  With ``gather`` (the
+    default) every rank returns the complete tree (a ``WaveletTree`` with the
+    CUDA ops); without, every rank returns its ``ShardedPart`` (distributed
+    output: no bitmap is all-gathered; ``assemble`` does it on demand)."""
+    part = _build_parts(S_local, sigma, comm, ops)
+    if not isinstance(part, ShardedPart):
+        return part
+    return assemble(part, comm, ops) if gather else part
+
+
+def _build_parts(S_local: torch.Tensor, sigma: int, comm=None, ops=None):
     comm = comm if comm is not None else TorchComm()
     ops = ops if ops is not None else CudaOps()
     P, r = comm.world, comm.rank
@@ -186,11 +234,10 @@ def build_sharded(S_local: torch.Tensor, sigma: int, comm=None, ops=None):
 
     # ---- 2: top levels of every chunk ----
     Tl = ops.build(ops.digits(S_local, shift, tau), ndig)
-    top_parts = comm.all_gather_v(_i64(Tl.bits).contiguous())
-    del Tl
 
     # ---- 3: exchange by digit, owners build levels >= tau ----
-    deep_parts, node_parts, no = [], [], np.zeros(P, dtype=np.int64)
+    no = np.zeros(P, dtype=np.int64)
+    To, R_o, n_o = None, 0, 0
     if L > tau:
         for o in range(P):
             no[o] = int(D[owner == o].sum())
@@ -205,6 +252,24 @@ def build_sharded(S_local: torch.Tensor, sigma: int, comm=None, ops=None):
         R_o = int(dstart[np.argmax(owner == r)]) if n_o else 0
         if n_o:
             To = ops.build(Ro, sigma)
+    return ShardedPart(rank=r, world=P, n=n, ns=ns, sigma=sigma, eb=eb, L=L, tau=tau, C=C, D=D, dstart=dstart,
+                       owner=owner, no=no, top=Tl, deep=To, R_o=R_o, n_o=n_o, device=dev)
+
+
+def assemble(part: ShardedPart, comm=None, ops=None):
+    """Step 4 of the sharded build: all-gather every rank's runs and nodes and
+    place them into the complete tree (on every rank)."""
+    comm = comm if comm is not None else TorchComm()
+    ops = ops if ops is not None else CudaOps()
+    P, r, n, ns, sigma, eb = part.world, part.rank, part.n, part.ns, part.sigma, part.eb
+    L, tau, C, D, dstart, owner, no, dev = (part.L, part.tau, part.C, part.D, part.dstart, part.owner,
+                                           part.no, part.device)
+    W = _wpl(n)
+    top_parts = comm.all_gather_v(_i64(part.top.bits).contiguous())
+    deep_parts, node_parts = [], []
+    if L > tau:
+        To, R_o, n_o = part.deep, part.R_o, part.n_o
+        if n_o:
             wo = _wpl(n_o)
             deep = _i64(To.bits)[tau * wo:].contiguous()
             lnp = _i64(To.level_node_ptr).cpu().numpy()
@@ -220,6 +285,7 @@ def build_sharded(S_local: torch.Tensor, sigma: int, comm=None, ops=None):
         deep_parts = comm.all_gather_v(deep)
         node_parts = [p.view(-1, 2) for p in comm.all_gather_v(packed)]
         node_cnts = [c.cpu().numpy() for c in comm.all_gather(lcnt)]  # [owner][level - tau]
+    part.free()
 
     # ---- 4: place every run, assemble the node table ----
     parts = top_parts + deep_parts

@@ -56,6 +56,18 @@ def _worker(rank, world, port, q, cases):
             lo, hi = int(cuts[rank]), int(cuts[rank + 1])
             t = wdist.build_sharded(torch.from_numpy(S[lo:hi].copy()), sigma, wdist.TorchComm(), HostOps())
             out.append(host_arrays(t))
+            # distributed output: the same parts assembled on demand give the same tree
+            part = wdist.build_sharded(torch.from_numpy(S[lo:hi].copy()), sigma, wdist.TorchComm(), HostOps(),
+                                       gather=False)
+            if isinstance(part, wdist.ShardedPart):
+                # this rank's top-level runs: lengths are its class counts, offsets inside the level
+                for k in range(part.tau):
+                    for p_, (off, ln) in part.place_top(k).items():
+                        assert 0 <= off and off + ln <= n
+                t2 = wdist.assemble(part, wdist.TorchComm(), HostOps())
+                out[-1] = (out[-1], host_arrays(t2))
+            else:
+                out[-1] = (out[-1], host_arrays(part))
         # invalid symbol on one rank only: every rank must raise
         bad = np.array([1, 2, 3] if rank == 0 else [1, 9, 2], dtype=np.uint8)
         try:
@@ -87,9 +99,9 @@ def test_sharded_build_gloo(world):
     for ci, (n, sigma, dtype, _) in enumerate(CASES):
         want = oracle.build(_seq(n, sigma, dtype, 100 + ci), sigma)
         for rank in range(world):
-            got = res[rank][ci]
-            for k in ("bits", "level_node_ptr", "node_key", "node_start", "rank_block", "rank_super"):
-                assert np.array_equal(got[k], want[k]), (ci, rank, k)
+            for got in res[rank][ci]:  # gathered build, distributed parts assembled
+                for k in ("bits", "level_node_ptr", "node_key", "node_start", "rank_block", "rank_super"):
+                    assert np.array_equal(got[k], want[k]), (ci, rank, k)
     for rank in range(world):
         assert res[rank][-1] == -2  # WT_ESYMBOL on every rank
 

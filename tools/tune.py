@@ -8,7 +8,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
-    "debug": ["WT_DEBUG=1"],
+    "base": [],
+    "tb16_6k": ["WT_CT_TB16=6144"],
+    "tb16_4k": ["WT_CT_TB16=4096"],
+    "u4": ["WT_WG_UNROLL=4"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
