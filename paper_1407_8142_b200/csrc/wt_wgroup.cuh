@@ -1,46 +1,57 @@
 // wt_wgroup.cuh -- the hot kernel, round 2: one HBM pass builds tau <= 8
 // consecutive levels l0 .. l0+tau-1 of the levelwise wavelet tree (SURVEY
-// §8(a) A2, A3, A5, A6), one independent WARP per chain.
+// §8(a) A2, A3, A5, A6, and A7's block counts), one CTA of CT_WARPS warps per
+// tile, persistent over chains.
 //
-// What a warp computes (Fig. 1 l.12-17, restated for a tile): a chain
+// What a CTA computes (Fig. 1 l.12-17, restated for a tile): a chain
 // is <= CH consecutive positions of S_{l0} inside one level-l0 node (its
-// "row"); it is processed in sub-tiles of <= T positions held in the warp's
-// own shared memory.  Inside a sub-tile the warp keeps the records in the
-// sub-tile's *wavelet-matrix order* M_k (the sub-tile stably sorted by the
-// reversed top-k digit bits): going from M_k to M_{k+1} is ONE
-// stable zeros-first split of the whole sub-tile by bit k, so no per-node
-// (per-class) split tables are needed.  A class of level k (the elements of
-// one level-(l0+k) node) is a contiguous run of M_k in
-// original order -- the same run it forms in S_{l0+k} --
-// so level l0+k's bitmap is M_k's bitmap with the class runs placed at their
-// tree positions.
+// "row"); it is processed in tiles of <= T positions held in shared memory.
+// Inside a tile the CTA keeps the records in the tile's *wavelet-matrix
+// order* M_k (the tile stably sorted by the reversed top-k digit bits,
+// PAPER.md:911-925): going from M_k to M_{k+1} is ONE stable zeros-first
+// split of the whole tile by bit k, so no per-node (per-class) split tables
+// are needed.  A class of level k (the elements of one level-(l0+k) node,
+// PAPER.md:213-226) is a contiguous run of M_k in original order -- the same
+// run it forms in S_{l0+k} -- so level l0+k's bitmap is
+// M_k's bitmap with the class runs placed at their tree positions.  Warp w
+// splits quarter w of the tile; the quarters' ones counts (onesW, from a
+// counting pass over the next bit) give each warp its zeros/ones bases, so a
+// level costs two CTA barriers.
 //
-// Records: rec = bit-reverse of the key over its kb = L - l0 remaining bits,
-// so the level-(l0+k) bit (the (l+1)'st highest bit) is rec bit
-// k and the reversed digit rd = rec & (2^tau - 1) is the class index r of
-// level tau in M_tau order.
+// Records: rec = bit-reverse of the top kb = min(L - l0, tau) key bits, plus
+// the remaining (payload) key bits above them in natural order, so the
+// level-(l0+k) bit (the (l+1)'st highest bit) is rec bit k, the
+// reversed digit rd = rec & (2^tau - 1) is the class index r of level tau in
+// M_tau order, and rec >> tau is the key narrowed for the next group.
 //
-// The split (per level, per 32*E-position "superchunk", E = 8 / sizeof(rec)):
-// lane l holds E consecutive records (one 8-byte LDS); the level bits t_j,
-// their exclusive in-lane prefix (SWAR: one IMAD per 4 bytes), the lane's
-// count and the cross-lane exclusive prefix O (ballots of the count's bits +
-// POPC) give every element its rank in its own stream; the destination is
+// The split (per level, per 32*E-position "superchunk", E = 8 (u8, u16
+// records) or 2 (u32)): lane l holds E consecutive records (one LDS.64 /
+// LDS.128); the level bits t_j, their exclusive in-lane prefix (SWAR: one IMAD
+// per 4 bytes), the lane's count and the cross-lane exclusive prefix O
+// (ballots of the count's bits + POPC) give every element its rank in its own
+// stream; the destination is
 //     bit 0: dst + zeros_before(superchunk) + (E*lane - O) + (j - pre_j)
 //     bit 1: dst + Z + ones_before(superchunk) + O + pre_j
 // (Fig. 1 l.15-17: zeros to start + X[i], ones to start + X_s + i - X[i]),
 // evaluated for two elements at a time with one dp2a each.  The level's
-// bitmap bytes and the ones-before count of every byte (a byte-grain rank
-// directory of the sub-tile) are written to shared memory; class counts of
-// level k+1 follow from rank queries at the class boundaries of level k, so
-// no per-tile digit histogram is built.  Padding records (all ones) fill the
+// bitmap bytes and the ones before every 32-bit word (a word-grain rank
+// directory of the tile) are written to shared memory; class counts of level
+// k+1 follow from rank queries at the class boundaries of level k, so no
+// per-tile digit histogram is built.  Padding records (all ones) fill the
 // last superchunk: they are ones at every level and stay at the end.
 //
+// Staging (north_star (2)): tile i+1's raw input (and, at a chain's last tile,
+// the next chain's starting digit counts V) is fetched by one cp.async.bulk
+// per tile into `stage`, completing on an mbarrier, while tile i is split.
+//
 // Global placement (A5): class r of level k goes to the
-// running position pos[slot], slot = 2^k + r, initialised per chain from the
-// chain tables (E, Cseg of wt_prep.cuh); words inside a run are stored, the
-// partial last word of a run is carried to the next sub-tile of the chain,
-// words shared with another chain or node are OR-ed atomically into the
-// zero-initialised bitmap.
+// running position pos[slot], slot = 2^k + r, initialised per chain from V
+// and the row's digit scan (Cseg of wt_prep.cuh); words inside a run are
+// stored, the partial last word of a run is carried to the next tile of the
+// chain, words shared with another chain or node are OR-ed atomically into
+// the zero-initialised bitmap.  Each run also adds its ones to the 512-bit
+// blocks it overlaps (red.add into blkcnt; fused A7), so the
+// rank directory needs no second read of the bitmaps (k_rank_counts).
 #pragma once
 #include "wt_common.cuh"
 #include "wt_group.cuh"  // GroupParams, CF_VALID / CF_SHARED
