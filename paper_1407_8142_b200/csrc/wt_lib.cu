@@ -53,7 +53,7 @@ GroupLaunch wgroup_launch() {
   return pd_.get([](GroupLaunch &gl) {
     gl.kern = k_wgroup<InT, RecT, OutT, HAS_OUT>;
     gl.smem = sizeof(WGSmem<InT, RecT, HAS_OUT>);
-    gl.tile = WGTile<RecT>::T;
+    gl.tile = WGSize<InT, RecT>::T;
     gl.threads = CT_WARPS * 32;
     cudaFuncSetAttribute(gl.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gl.smem);
     int per_sm = 0;
@@ -113,6 +113,7 @@ LocalLaunch pick_local(uint32_t inw, uint32_t recw, uint32_t outw, bool has_out)
     return LocalLaunch{};
   }
   if (recw == 2) {
+    if (outw == 2) return LocalLaunch{};  // not instantiated (WT_TAUS splits only): build reports WT_EUNSUPPORTED
     if (inw == 2) return local_launch<uint16_t, uint16_t, uint8_t, true>();
     return local_launch<uint32_t, uint16_t, uint8_t, true>();
   }
@@ -131,7 +132,12 @@ GroupLaunch pick_group_mode(uint32_t inw, uint32_t recw, uint32_t outw, bool has
     }
     return GroupLaunch{};  // the last group always has <= 8 bits per record
   }
+  if (recw == 1) return GroupLaunch{};  // 8-bit records with a payload: not instantiated (WT_TAUS splits only)
   if (recw == 2) {
+    if (outw == 2) {  // tau < 8 with a payload of 9..15 bits (WT_TAUS splits)
+      if (inw == 2) return wgroup_launch<uint16_t, uint16_t, uint16_t, true>();
+      return wgroup_launch<uint32_t, uint16_t, uint16_t, true>();
+    }
     if (inw == 2) return any_group_launch<uint16_t, uint16_t, uint8_t, true>();
     return any_group_launch<uint32_t, uint16_t, uint8_t, true>();
   }
@@ -244,12 +250,32 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   // one or two levels (sigma <= 4): the direct kernels of wt_small.cuh
   const bool small = (L == 1 || L == 2) && n > 0 && eb == 1 && !getenv("WT_NO_SMALL") &&
                      (from_host || reinterpret_cast<uintptr_t>(d_seq) % 16 == 0);
-  const uint32_t NG = small ? 0u : (L + TAU_MAX - 1) / TAU_MAX;
-  GroupBufs G[4];
-  for (uint32_t g = 0; g < NG; g++) {
+  // levels per group: tau = 8 greedily (the last group takes the rest); WT_TAUS="a,b,..."
+  // (developer knob, used only when the list sums to L) overrides the split
+  uint32_t taus[8] = {0}, NG = 0;
+  if (!small) {
+    if (const char *e = getenv("WT_TAUS")) {
+      uint32_t sum = 0, k = 0;
+      for (const char *c = e; *c && k < 8;) {
+        const uint32_t v = (uint32_t)strtoul(c, (char **)&c, 10);
+        if (v < 1 || v > TAU_MAX) { k = 0; break; }
+        taus[k++] = v;
+        sum += v;
+        if (*c == ',') c++;
+        else break;
+      }
+      if (sum == L && k) NG = k;
+    }
+    if (!NG) {
+      NG = (L + TAU_MAX - 1) / TAU_MAX;
+      for (uint32_t g = 0; g < NG; g++) taus[g] = std::min<uint32_t>(TAU_MAX, L - g * TAU_MAX);
+    }
+  }
+  GroupBufs G[8];
+  for (uint32_t g = 0, l0 = 0; g < NG; l0 += taus[g], g++) {
     GroupBufs &gb = G[g];
-    gb.l0 = g * TAU_MAX;
-    gb.tau = std::min<uint32_t>(TAU_MAX, L - gb.l0);
+    gb.l0 = l0;
+    gb.tau = taus[g];
     gb.pbits = L - gb.l0 - gb.tau;
     gb.ndig = 1u << gb.tau;
     gb.k_lo = g == 0 ? 0u : 1u;

@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
   const uint32_t tau = p.tau, pbits = p.pbits, ndig = 1u << tau;
   const uint32_t pmask = (1u << pbits) - 1u;
   const uint32_t nrows = p.counts[1];
+  const uint32_t nk = p.nk;
   const uint32_t lt = lanemask_lt();
 
   while (true) {
@@ -158,6 +159,20 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
     if (lane < (int)p.nk)
       nodeoff = COUNT ? 0u : (MODE == LM_BIG ? p.defer[(uint64_t)b * DEFER_W + 1 + lane]
                                              : p.batchcnt[(uint64_t)lane * p.nbatch + b]);
+    // lane kk (< nk): the global index of the next node of level l0+1+kk
+    uint64_t gn = 0;
+    if (!COUNT && lane < (int)p.nk) gn = p.level_node_ptr[p.l0 + 1 + lane] + nodeoff;
+    uint32_t gn_lo = (uint32_t)gn, gn_hi = (uint32_t)(gn >> 32);
+    auto node_add = [&](uint32_t c) {  // lane kk: c more nodes of level l0+1+kk
+      if (lane < (int)nk) {
+        nodeoff += c;
+        if (!COUNT) {
+          gn += c;
+          gn_lo = (uint32_t)gn;
+          gn_hi = (uint32_t)(gn >> 32);
+        }
+      }
+    };
     __syncwarp();
 
     // the next row's start, key and first 64 symbols are loaded one row ahead
@@ -176,13 +191,20 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
       }
       if (len <= 32) {
         // ---------------- register path ----------------
+        // rd: the symbol's tau digit bits reversed, so that local level k's bit
+        // (the (k+1)'st highest) is rd bit k; the loop is unrolled
+        // over k (constant shifts, constant lane selects)
         const bool valid = (uint32_t)lane < len;
         const uint32_t key = valid ? kA0 : 0u;
         const uint32_t dig = (key >> pbits) & (ndig - 1u);
+        const uint32_t rd = __brev(dig) >> (32u - tau);
         uint32_t eq = __ballot_sync(FULL, valid), ltm = 0;  // same prefix / smaller prefix (this row)
         uint32_t myw = 0;                                    // lane k: the row's word of level l0+k
-        for (uint32_t k = 0; k < tau; k++) {
-          const uint32_t bit = (dig >> (tau - 1u - k)) & 1u;
+        uint32_t cpk0 = 0, cpk1 = 0;                         // node counts of levels l0+1.., 8 bits each
+#pragma unroll
+        for (uint32_t k = 0; k < TAU_MAX; k++) {
+          if (k >= tau) break;
+          const uint32_t bit = (rd >> k) & 1u;
           const uint32_t m = __ballot_sync(FULL, valid && bit);
           if (!COUNT) {
             const uint32_t pos = __popc(ltm) + __popc(eq & lt);  // position at level l0+k
@@ -196,18 +218,22 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
           } else {
             eq &= ~m;
           }
-          if (k + 1 <= p.nk) {  // nodes of level l0+k+1 = distinct (k+1)-bit prefixes
+          if (k + 1 <= nk) {  // nodes of level l0+k+1 = distinct (k+1)-bit prefixes
             const bool first = valid && (eq & lt) == 0;
             const uint32_t fm = __ballot_sync(FULL, first);
-            const uint32_t base = __shfl_sync(FULL, nodeoff, k);  // lane k holds level l0+k+1
-            if (!COUNT && first) {
-              const uint64_t j = p.level_node_ptr[p.l0 + k + 1] + base + __popc(fm & ltm);  // leaders with a smaller prefix
-              p.node_key[j] = (P << (k + 1)) | (dig >> (tau - 1u - k));
-              p.node_start[j] = rs + __popc(ltm);
+            if (!COUNT) {
+              const uint64_t j0 = ((uint64_t)__shfl_sync(FULL, gn_hi, k) << 32) | __shfl_sync(FULL, gn_lo, k);
+              if (first) {
+                const uint64_t j = j0 + __popc(fm & ltm);  // leaders with a smaller prefix
+                p.node_key[j] = (P << (k + 1)) | (dig >> (tau - 1u - k));
+                p.node_start[j] = rs + __popc(ltm);
+              }
             }
-            if (lane == (int)k) nodeoff += __popc(fm);
+            if (k < 4) cpk0 += __popc(fm) << (8 * k);
+            else cpk1 += __popc(fm) << (8 * (k - 4));
           }
         }
+        node_add(((lane & 4) ? cpk1 : cpk0) >> (8 * (lane & 3)) & 0xffu);
         if (HAS_OUT && !COUNT && valid) ko[rs + __popc(ltm) + __popc(eq & lt)] = (OutT)(key & pmask);
         if (!COUNT && lane < (int)tau) acc_put(ws, lane, rs, myw, len, Bl, A, Bend, p.n);
         __syncwarp();
@@ -217,35 +243,36 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
         // ---------------- register path, two symbols per lane ----------------
         // symbols x = lane (A) and x = 32 + lane (B); 64-bit masks over the row:
         // eq = same prefix as x, ltm = smaller prefix than x, before = index < x.
-        const bool vA = true, vB = (uint32_t)lane + 32u < len;
+        const bool vB = (uint32_t)lane + 32u < len;
         const uint32_t kA = kA0;
         const uint32_t kB = vB ? kB0 : 0u;
         const uint32_t dA = (kA >> pbits) & (ndig - 1u), dB = (kB >> pbits) & (ndig - 1u);
+        const uint32_t rA = __brev(dA) >> (32u - tau), rB = __brev(dB) >> (32u - tau);
         const uint64_t valid64 = ((uint64_t)__ballot_sync(FULL, vB) << 32) | 0xffffffffull;
         const uint64_t befA = (uint64_t)lt, befB = 0xffffffffull | ((uint64_t)lt << 32);
         uint64_t eqA = valid64, eqB = valid64, ltA = 0, ltB = 0;
         uint32_t mylo = 0, myhi = 0;  // lane k: the row's words of level l0+k
-        for (uint32_t k = 0; k < tau; k++) {
-          const uint32_t bA = (dA >> (tau - 1u - k)) & 1u, bB = (dB >> (tau - 1u - k)) & 1u;
-          const uint64_t M = ((uint64_t)__ballot_sync(FULL, vB && bB) << 32) | __ballot_sync(FULL, vA && bA);
+        uint32_t cpk0 = 0, cpk1 = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < TAU_MAX; k++) {
+          if (k >= tau) break;
+          const uint32_t bA = (rA >> k) & 1u, bB = (rB >> k) & 1u;
+          const uint64_t M = ((uint64_t)__ballot_sync(FULL, vB && bB) << 32) | __ballot_sync(FULL, bA);
           if (!COUNT) {
             const uint32_t pA = __popcll(ltA) + __popcll(eqA & befA);
             const uint32_t pB = __popcll(ltB) + __popcll(eqB & befB);
-            uint32_t lo = 0, hi = 0;
-            if (bA) { if (pA < 32) lo |= 1u << pA; else hi |= 1u << (pA - 32); }
-            if (vB && bB) { if (pB < 32) lo |= 1u << pB; else hi |= 1u << (pB - 32); }
-            lo = __reduce_or_sync(FULL, lo);
-            hi = __reduce_or_sync(FULL, hi);
+            const uint32_t oA = bA ? 1u << (pA & 31u) : 0u, oB = (vB && bB) ? 1u << (pB & 31u) : 0u;
+            const uint32_t lo = __reduce_or_sync(FULL, (pA < 32 ? oA : 0u) | (pB < 32 ? oB : 0u));
+            const uint32_t hi = __reduce_or_sync(FULL, (pA < 32 ? 0u : oA) | (pB < 32 ? 0u : oB));
             if (lane == (int)k) { mylo = lo; myhi = hi; }
           }
           if (bA) { ltA |= eqA & ~M; eqA &= M; } else { eqA &= ~M; }
           if (bB) { ltB |= eqB & ~M; eqB &= M; } else { eqB &= ~M; }
-          if (k + 1 <= p.nk) {  // nodes of level l0+k+1 = distinct (k+1)-bit prefixes
+          if (k + 1 <= nk) {  // nodes of level l0+k+1 = distinct (k+1)-bit prefixes
             const bool fA = (eqA & befA) == 0, fB = vB && (eqB & befB) == 0;
             const uint64_t F = ((uint64_t)__ballot_sync(FULL, fB) << 32) | __ballot_sync(FULL, fA);
-            const uint32_t base = __shfl_sync(FULL, nodeoff, k);
             if (!COUNT) {
-              const uint64_t j0 = p.level_node_ptr[p.l0 + k + 1] + base;
+              const uint64_t j0 = ((uint64_t)__shfl_sync(FULL, gn_hi, k) << 32) | __shfl_sync(FULL, gn_lo, k);
               if (fA) {
                 p.node_key[j0 + __popcll(F & ltA)] = (P << (k + 1)) | (dA >> (tau - 1u - k));
                 p.node_start[j0 + __popcll(F & ltA)] = rs + __popcll(ltA);
@@ -255,9 +282,11 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
                 p.node_start[j0 + __popcll(F & ltB)] = rs + __popcll(ltB);
               }
             }
-            if (lane == (int)k) nodeoff += __popcll(F);
+            if (k < 4) cpk0 += __popcll(F) << (8 * k);
+            else cpk1 += __popcll(F) << (8 * (k - 4));
           }
         }
+        node_add(((lane & 4) ? cpk1 : cpk0) >> (8 * (lane & 3)) & 0xffu);
         if (HAS_OUT && !COUNT) {
           ko[rs + __popcll(ltA) + __popcll(eqA & befA)] = (OutT)(kA & pmask);
           if (vB) ko[rs + __popcll(ltB) + __popcll(eqB & befB)] = (OutT)(kB & pmask);
@@ -325,6 +354,11 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
           base += __popc(bm);
         }
         if (lane == (int)(k - 1)) nodeoff = base;
+      }
+      if (!COUNT && lane < (int)nk) {  // keep the node cursors of the register paths in step
+        gn = p.level_node_ptr[p.l0 + 1 + lane] + nodeoff;
+        gn_lo = (uint32_t)gn;
+        gn_hi = (uint32_t)(gn >> 32);
       }
       if (!COUNT && emit) {
       for (uint32_t k = 0; k < tau; k++) {

@@ -71,25 +71,49 @@ template <typename RecT>
 struct WGTile {
   static constexpr int E = sizeof(RecT) == 4 ? 2 : 8;  // records per lane per superchunk (one LDS)
   static constexpr int SC = 32 * E;                      // positions per superchunk
+};
+
+#ifndef WT_WG_STAGE32
+#define WT_WG_STAGE32 0
+#endif
+// whether tiles of this input width are prefetched into shared memory by a bulk
+// copy (else the load step reads them from global memory directly)
+template <typename InT>
+struct WGStage {
+  static constexpr bool on = sizeof(InT) < 4 || WT_WG_STAGE32;
+};
+
 #ifndef WT_CT_TB
 #define WT_CT_TB 8192
 #endif
 #ifndef WT_CT_TB16
 #define WT_CT_TB16 6144
 #endif
-  // records per tile (WT_CT_TB bytes of records; WT_CT_TB16 for 16-bit records)
-  static constexpr int T = (sizeof(RecT) == 2 ? WT_CT_TB16 : WT_CT_TB) / (int)sizeof(RecT);
-  static constexpr int SPW = T / SC / CT_WARPS;           // superchunks per warp
-  static_assert(SPW >= 1 && T % (SC * CT_WARPS) == 0, "whole superchunks per warp");
+#ifndef WT_CT_TB16NS
+#define WT_CT_TB16NS 12288
+#endif
+#ifndef WT_CT_TB32NS
+#define WT_CT_TB32NS 8192
+#endif
+// records per tile: WT_CT_TB bytes of records (WT_CT_TB16 for 16-bit records of a staged
+// input; the unstaged 32-bit inputs have the stage's shared memory for larger tiles)
+template <typename InT, typename RecT>
+struct WGSize {
+  static constexpr int RB = sizeof(RecT);
+  static constexpr int BYTES = RB == 2 ? (WGStage<InT>::on ? WT_CT_TB16 : WT_CT_TB16NS)
+                                       : (RB == 4 && !WGStage<InT>::on ? WT_CT_TB32NS : WT_CT_TB);
+  static constexpr int T = BYTES / RB;
+  static constexpr int SPW = T / WGTile<RecT>::SC / CT_WARPS;  // superchunks per warp
+  static_assert(SPW >= 1 && T % (WGTile<RecT>::SC * CT_WARPS) == 0, "whole superchunks per warp");
 };
 
 template <typename InT, typename RecT, bool HAS_OUT>
 struct WGSmem {
-  static constexpr int T = WGTile<RecT>::T;
+  static constexpr int T = WGSize<InT, RecT>::T;
   static constexpr int LBB = T / 8 + 16;  // bytes per level bitmap (+ slack for 3-word reads)
   static constexpr int RPW = T / 32 + 2;  // word ranks per level (+ the padded end)
   alignas(16) RecT rec[2][T];
-  alignas(16) uint8_t stage[T * sizeof(InT) + 32];  // raw input of the next tile (TMA bulk copy)
+  alignas(16) uint8_t stage[WGStage<InT>::on ? T * sizeof(InT) + 32 : 16];  // raw input of the next tile (TMA bulk copy)
   alignas(16) uint8_t LB[TAU_MAX][LBB];  // level bitmaps of the tile (M_k order)
   alignas(16) uint16_t RP[TAU_MAX][RPW]; // ones of the level before each 32-bit word of LB
   alignas(16) uint32_t V[256];           // chain's starting digit counts (bulk copy, next chain's)
@@ -436,13 +460,42 @@ __device__ __forceinline__ void stage_words(const uint8_t *stg, uint32_t g, uint
 #undef WG_SHIFT
 }
 
+// as stage_words, from global memory (V = the 16-byte-aligned cover of the tile)
+template <uint32_t NV>
+__device__ __forceinline__ void global_words(const uint4 *V0, uint32_t g, uint32_t h, uint32_t *in) {
+  const uint4 *V = V0 + NV * g;
+  uint32_t raw[4 * NV + 4];
+#pragma unroll
+  for (uint32_t q = 0; q < NV; q++) {
+    const uint4 u = __ldcs(V + q);
+    raw[4 * q] = u.x; raw[4 * q + 1] = u.y; raw[4 * q + 2] = u.z; raw[4 * q + 3] = u.w;
+  }
+  if (h == 0) {
+#pragma unroll
+    for (uint32_t q = 0; q < 4 * NV; q++) in[q] = raw[q];
+    return;
+  }
+  {
+    const uint4 u = __ldcs(V + NV);
+    raw[4 * NV] = u.x; raw[4 * NV + 1] = u.y; raw[4 * NV + 2] = u.z; raw[4 * NV + 3] = u.w;
+  }
+  const uint32_t hb = 8u * (h & 3u);
+#define WG_SHIFT(H)                                                                                             \
+  case H:                                                                                                       \
+    _Pragma("unroll") for (uint32_t q = 0; q < 4 * NV; q++) in[q] = __funnelshift_r(raw[q + H], raw[q + H + 1], hb); \
+    break;
+  switch (h >> 2) { WG_SHIFT(0) WG_SHIFT(1) WG_SHIFT(2) WG_SHIFT(3) }
+#undef WG_SHIFT
+}
+
 template <typename InT, typename RecT, typename OutT, bool HAS_OUT>
 __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
   using SM = WGSmem<InT, RecT, HAS_OUT>;
-  constexpr uint32_t T = SM::T, SC = WGTile<RecT>::SC, SPW = WGTile<RecT>::SPW, RB = sizeof(RecT),
+  constexpr uint32_t T = SM::T, SC = WGTile<RecT>::SC, SPW = WGSize<InT, RecT>::SPW, RB = sizeof(RecT),
                      IB = sizeof(InT);
   constexpr uint32_t PER = 16 / RB, NV = PER * IB / 16;  // records per 16-byte group, input uint4 per group
   constexpr uint32_t NT = CT_WARPS * 32;
+  constexpr bool STAGE = WGStage<InT>::on;
   extern __shared__ __align__(16) uint8_t wg_raw[];
   SM &s = *reinterpret_cast<SM *>(wg_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -460,7 +513,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
     const uint32_t c = atomicAdd(p.chain_counter, 1u);
     if (c < nchains) {
       const uint32_t b = p.chain_begin[c], e = p.chain_end[c];
-      bulk_load2(stg, keys + b, min(e - b, T) * IB, vA, p.V + (uint64_t)c * 256, 1024u, bar);
+      if constexpr (STAGE) bulk_load2(stg, keys + b, min(e - b, T) * IB, vA, p.V + (uint64_t)c * 256, 1024u, bar);
+      else bulk_load(vA, p.V + (uint64_t)c * 256, 1024u, bar);
     }
     return c;
   };
@@ -480,6 +534,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
     const uint32_t *Cg = p.Cseg + (uint64_t)row * (ndig + 1);
     uint32_t *X = reinterpret_cast<uint32_t *>(s.CW);  // scratch until the carries start
     bar_wait(bar, phase);  // the chain's digit vector (and first tile) have landed
+    if constexpr (!STAGE) phase ^= 1u;  // one bulk copy (V) per chain
     if (warp == 0) {
       // X[d] = exclusive scan over digits of the same-row elements ahead of the chain
       uint32_t v[8], sum = 0;
@@ -524,8 +579,10 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
       // ---- 1. records from the staged input + ones of bit 0 per quarter ----
       // record = (payload << tau) | reversed digit: level l0+k's bit (the (k+1)'st highest
       // bit of the key) is record bit k; the payload keeps its natural order
-      if (start64 != cbeg) bar_wait(bar, phase);
-      phase ^= 1u;
+      if constexpr (STAGE) {
+        if (start64 != cbeg) bar_wait(bar, phase);
+        phase ^= 1u;
+      }
       {
         const uint32_t h = (uint32_t)(reinterpret_cast<uintptr_t>(keys + start) & 15u);
         RecT *R = s.rec[0];
@@ -533,7 +590,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
         for (uint32_t g = c0 * (SC / PER) + lane; g < c1 * (SC / PER); g += 32) {
           const uint32_t i0 = g * PER;
           uint32_t in[4 * NV], w[4];
-          stage_words<NV>(s.stage, g, h, in);
+          if constexpr (STAGE) stage_words<NV>(s.stage, g, h, in);
+          else global_words<NV>(reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(keys + start) & ~(uintptr_t)15), g, h, in);
           if constexpr (IB == 1 && RB == 1) {
 #pragma unroll
             for (int q = 0; q < 4; q++) {
@@ -592,8 +650,13 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
       __syncthreads();
       // the staging buffer is free: prefetch the next tile of the chain, or the next chain's first
       if (tid == 0) {
-        if (start64 + T < cend) bulk_load(stg, keys + start + T, min(cend - (start + T), T) * IB, bar);
-        else s.cnext = claim();
+        if (!STAGE) {
+          if (start64 + T >= cend) s.cnext = claim();
+        } else if (start64 + T < cend) {
+          bulk_load(stg, keys + start + T, min(cend - (start + T), T) * IB, bar);
+        } else {
+          s.cnext = claim();
+        }
       }
 
       // ---- 2. tau levels of splits (bitmaps and word ranks kept per level) ----

@@ -9,9 +9,9 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
     "base": [],
-    "tb16_6k": ["WT_CT_TB16=6144"],
-    "tb16_4k": ["WT_CT_TB16=4096"],
-    "u4": ["WT_WG_UNROLL=4"],
+    "t32ns_4k": ["WT_CT_TB32NS=16384"],
+    "t32ns_2k": ["WT_CT_TB32NS=8192", "WT_CT_TB16NS=10240"],
+    "t16ns_8k": ["WT_CT_TB16NS=16384"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
