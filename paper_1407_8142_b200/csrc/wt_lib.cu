@@ -345,12 +345,48 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
 
   chk(cudaMemsetAsync(err, 0, 4 * sizeof(uint32_t), s));
   chk(cudaMemsetAsync(t->level_node_ptr, 0, (L + 1) * sizeof(uint64_t), s));
-  if (L && n) chk(cudaMemsetAsync(t->bits, 0, L * WPL * sizeof(uint64_t), s));
-  if (blkcnt) chk(cudaMemsetAsync(blkcnt, 0, (uint64_t)L * BPL * sizeof(uint32_t), s));
   for (uint32_t g = 0; g < NG; g++) chk(cudaMemsetAsync(G[g].counts, 0, 4 * sizeof(uint32_t), s));
+  cudaStream_t side = side_stream();
+  // Zeroing of the bitmaps (and of the fused-A7 block counts): with level groups, one
+  // memset per group on the side stream, so that it overlaps the prep kernels and the
+  // earlier (compute-bound) group passes; group g's first bitmap writer waits for
+  // ev_zero[g].  The side stream first waits for this stream (the allocations).
+  cudaEvent_t ev_zero[8] = {};
+  bool zeroed[8] = {};
+  const bool zero_side = L && n && NG > 0;
+  // group g's levels: zeroed on the side stream once this stream reaches this point
+  auto zero_group = [&](uint32_t g) {
+    if (!zero_side || g >= NG || zeroed[g]) return;
+    zeroed[g] = true;
+    cudaEvent_t ev0;
+    chk(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+    chk(cudaEventRecord(ev0, s));
+    chk(cudaStreamWaitEvent(side, ev0, 0));
+    cudaEventDestroy(ev0);
+    chk(cudaMemsetAsync(t->bits + (uint64_t)G[g].l0 * WPL, 0, (uint64_t)G[g].tau * WPL * sizeof(uint64_t), side));
+    if (blkcnt)
+      chk(cudaMemsetAsync(blkcnt + (uint64_t)G[g].l0 * BPL, 0, (uint64_t)G[g].tau * BPL * sizeof(uint32_t), side));
+    chk(cudaEventCreateWithFlags(&ev_zero[g], cudaEventDisableTiming));
+    chk(cudaEventRecord(ev_zero[g], side));
+  };
+  if (zero_side) {
+    // all groups now: the memsets overlap A1 and the chain setup (measured: a memset
+    // running next to a persistent group pass takes its SM slots and slows it more)
+    for (uint32_t g = 0; g < NG; g++) zero_group(g);
+  } else {
+    if (L && n) chk(cudaMemsetAsync(t->bits, 0, L * WPL * sizeof(uint64_t), s));
+    if (blkcnt) chk(cudaMemsetAsync(blkcnt, 0, (uint64_t)L * BPL * sizeof(uint32_t), s));
+  }
+  auto wait_zero = [&](uint32_t g) {
+    if (g < NG) zero_group(g);  // (no-op when already enqueued)
+    if (g < 8 && ev_zero[g]) {
+      chk(cudaStreamWaitEvent(s, ev_zero[g], 0));
+      cudaEventDestroy(ev_zero[g]);
+      ev_zero[g] = nullptr;
+    }
+  };
 
   // A7 per level group, on the side stream once the group's bitmaps are final
-  cudaStream_t side = side_stream();
   cudaEvent_t ev_side = nullptr;
   bool side_used = false;
   // (the last group's directory has no later pass to overlap: main stream)
@@ -485,6 +521,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       char name[32];
       snprintf(name, sizeof(name), "k_group%u", g);
       rec.begin(name, (uint64_t)gb.tau * WPL * 8);  // algorithmic: the group's bitmap levels
+      wait_zero(g);
       gb.ll.build<<<gb.ll.grid, LOCAL_WARPS * 32, gb.ll.smem, s>>>(lp);
       chk(cudaGetLastError());
       chk(cudaMemsetAsync(gb.bcounts, 0, sizeof(uint32_t), s));  // claim counter for the deferred rows
@@ -594,6 +631,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     // algorithmic bytes: S read once (group 0) + the group's bitmap
     // levels; the narrowed keys between groups are overhead, not counted
     rec.begin(name, (g == 0 ? n * eb : 0) + (uint64_t)gb.tau * WPL * 8);
+    wait_zero(g);
     gb.gl.kern<<<gb.gl.grid, gb.gl.threads, gb.gl.smem, s>>>(gp);
     chk(cudaGetLastError());
     rec.end();
@@ -630,6 +668,12 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   }
 
   if (ev_side) cudaEventDestroy(ev_side);
+  for (uint32_t g = 0; g < 8; g++) {  // groups that never launched (errors): keep s ordered
+    if (ev_zero[g]) {
+      chk(cudaStreamWaitEvent(s, ev_zero[g], 0));
+      cudaEventDestroy(ev_zero[g]);
+    }
+  }
   // ---- the single host sync: error flag + node count ----
   chk(cudaMemcpyAsync(h_stage, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   if (L) chk(cudaMemcpyAsync(h_stage + 1, t->level_node_ptr + L, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));

@@ -420,6 +420,13 @@ __device__ __forceinline__ void bulk_load2(uint32_t dst, const void *src, uint32
                "l"(src2), "r"(bytes2), "r"(bar)
                : "memory");
 }
+// bulk prefetch of [src, src + bytes) into L2 (TMA unit; the 16-byte-aligned cover)
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + bytes + 15) & ~(uintptr_t)15;
+  if (a1 > a0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+}
 __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {
@@ -513,8 +520,12 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
     const uint32_t c = atomicAdd(p.chain_counter, 1u);
     if (c < nchains) {
       const uint32_t b = p.chain_begin[c], e = p.chain_end[c];
-      if constexpr (STAGE) bulk_load2(stg, keys + b, min(e - b, T) * IB, vA, p.V + (uint64_t)c * 256, 1024u, bar);
-      else bulk_load(vA, p.V + (uint64_t)c * 256, 1024u, bar);
+      if constexpr (STAGE) {
+        bulk_load2(stg, keys + b, min(e - b, T) * IB, vA, p.V + (uint64_t)c * 256, 1024u, bar);
+      } else {
+        bulk_load(vA, p.V + (uint64_t)c * 256, 1024u, bar);
+        prefetch_l2(keys + b, min(e - b, T) * IB);  // the chain's first tile, read at its start
+      }
     }
     return c;
   };
@@ -650,8 +661,9 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
       __syncthreads();
       // the staging buffer is free: prefetch the next tile of the chain, or the next chain's first
       if (tid == 0) {
-        if (!STAGE) {
-          if (start64 + T >= cend) s.cnext = claim();
+        if (!STAGE) {  // the next tile of the chain into L2 while this one is split
+          if (start64 + T < cend) prefetch_l2(keys + start + T, min(cend - (start + T), T) * IB);
+          else s.cnext = claim();
         } else if (start64 + T < cend) {
           bulk_load(stg, keys + start + T, min(cend - (start + T), T) * IB, bar);
         } else {
