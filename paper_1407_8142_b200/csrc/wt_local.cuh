@@ -72,6 +72,7 @@ struct LocalSmem {
   uint32_t accw[TAU_MAX];           // ... and its index (rows arrive in position order)
   alignas(16) uint32_t LB[MODE == LM_COUNT ? 1 : BUFN / 32];
   uint32_t hist2[NDIG / 2];
+  uint32_t pres[NDIG / 32];  // counting pass: the digits present in a row (bit set)
   uint16_t Hl[NDIG + 2];
   uint16_t T[NDIG];
 };
@@ -188,6 +189,50 @@ __global__ void __launch_bounds__(LOCAL_WARPS * 32) k_local(LocalParams p) {
         P_n = p.row_key[r + 1];
         kA_n = (uint64_t)rs_n + lane < p.n ? (uint32_t)keys[(uint64_t)rs_n + lane] : 0u;
         kB_n = (uint64_t)rs_n + 32 + lane < p.n ? (uint32_t)keys[(uint64_t)rs_n + 32 + lane] : 0u;
+      }
+      if (COUNT && len <= 64) {
+        // ---------------- counting pass, rows of <= 64 symbols ----------------
+        // nodes of level l0+k = the distinct k-bit digit prefixes of the row (Fig. 1
+        // l.18-20): with the row's digit set as a bitmap (one shared-memory OR per
+        // symbol), a k-bit prefix is a group of 2^(tau-k) consecutive bits, and the
+        // count is the number of non-empty groups (bit folds + POPC per word)
+        const uint32_t nw = (ndig + 31) >> 5;
+        if (lane < (int)nw) ws.pres[lane] = 0;
+        __syncwarp();
+        const uint32_t dA = (kA0 >> pbits) & (ndig - 1u), dB = (kB0 >> pbits) & (ndig - 1u);
+        if ((uint32_t)lane < len) atomicOr(&ws.pres[dA >> 5], 1u << (dA & 31u));
+        if ((uint32_t)lane + 32u < len) atomicOr(&ws.pres[dB >> 5], 1u << (dB & 31u));
+        __syncwarp();
+        uint32_t y = lane < (int)nw ? ws.pres[lane] : 0u;
+        const uint32_t wm = __ballot_sync(FULL, y != 0);  // non-empty 32-digit words
+        // c_G = non-empty groups of 2^G digits, G = 0..5, per word; three 10-bit fields per sum
+        uint32_t c012 = __popc(y);
+        y |= y >> 1;
+        c012 |= __popc(y & 0x55555555u) << 10;
+        y |= y >> 2;
+        c012 |= __popc(y & 0x11111111u) << 20;
+        y |= y >> 4;
+        uint32_t c345 = __popc(y & 0x01010101u);
+        y |= y >> 8;
+        c345 |= __popc(y & 0x00010001u) << 10;
+        y |= y >> 16;
+        c345 |= (y & 1u) << 20;
+        c012 = __reduce_add_sync(FULL, c012);
+        c345 = __reduce_add_sync(FULL, c345);
+        // lane j: level l0+1+j, groups of 2^G digits with G = tau - 1 - j
+        const int G = (int)tau - 1 - lane;
+        uint32_t cnt = 0;
+        if (G >= 0 && G <= 2) cnt = (c012 >> (10 * G)) & 1023u;
+        else if (G >= 3 && G <= 5) cnt = (c345 >> (10 * (G - 3))) & 1023u;
+        else if (G >= 6) {  // groups of 2^(G-5) words
+          const uint32_t gw = 1u << (G - 5);
+          uint32_t m = wm;
+          for (uint32_t sh = 1; sh < gw; sh <<= 1) m |= m >> sh;
+          cnt = __popc(m & (gw == 2 ? 0x55u : (gw == 4 ? 0x11u : 0x01u)));
+        }
+        node_add(cnt);
+        __syncwarp();
+        continue;
       }
       if (len <= 32) {
         // ---------------- register path ----------------
