@@ -40,9 +40,13 @@
 // per-tile digit histogram is built.  Padding records (all ones) fill the
 // last superchunk: they are ones at every level and stay at the end.
 //
-// Staging (north_star (2)): tile i+1's raw input (and, at a chain's last tile,
-// the next chain's starting digit counts V) is fetched by one cp.async.bulk
-// per tile into `stage`, completing on an mbarrier, while tile i is split.
+// Staging (north_star (2)): for 8-bit inputs (the 8-bit digit passes) tile
+// i+1's raw input (and, at a chain's last tile, the next chain's starting digit
+// counts V) is fetched by one cp.async.bulk per tile into `stage`, completing on
+// an mbarrier, while tile i is split.  16/32-bit inputs skip the stage (its
+// 2-4 B per position of shared memory buy larger tiles instead, measured
+// faster): the load step reads them with 16-byte loads, and the TMA unit
+// prefetches the next tile into L2 (cp.async.bulk.prefetch.L2) meanwhile.
 //
 // Global placement (A5): class r of level k goes to the
 // running position pos[slot], slot = 2^k + r, initialised per chain from V
@@ -78,9 +82,15 @@ struct WGTile {
 #endif
 // whether tiles of this input width are prefetched into shared memory by a bulk
 // copy (else the load step reads them from global memory directly)
+#ifndef WT_WG_STAGE16
+#define WT_WG_STAGE16 0
+#endif
+#ifndef WT_WG_STAGE8
+#define WT_WG_STAGE8 1
+#endif
 template <typename InT>
 struct WGStage {
-  static constexpr bool on = sizeof(InT) < 4 || WT_WG_STAGE32;
+  static constexpr bool on = sizeof(InT) == 1 ? WT_WG_STAGE8 : sizeof(InT) == 2 ? WT_WG_STAGE16 : WT_WG_STAGE32;
 };
 
 #ifndef WT_CT_TB
@@ -96,12 +106,22 @@ struct WGStage {
 #define WT_CT_TB32NS 8192
 #endif
 // records per tile: WT_CT_TB bytes of records (WT_CT_TB16 for 16-bit records of a staged
-// input; the unstaged 32-bit inputs have the stage's shared memory for larger tiles)
+// input); unstaged inputs use the stage's shared memory for larger tiles: 6144
+// 16-bit records of a 32-bit input, 4096 of a 16-bit input, 2048 32-bit records
+// (tools/tune.py).  8-bit inputs (the 8-bit digit passes) stay
+// TMA-staged: one cp.async.bulk per tile, one tile ahead.
 template <typename InT, typename RecT>
 struct WGSize {
   static constexpr int RB = sizeof(RecT);
-  static constexpr int BYTES = RB == 2 ? (WGStage<InT>::on ? WT_CT_TB16 : WT_CT_TB16NS)
-                                       : (RB == 4 && !WGStage<InT>::on ? WT_CT_TB32NS : WT_CT_TB);
+#ifndef WT_CT_TBNS
+#define WT_CT_TBNS WT_CT_TB
+#endif
+#ifndef WT_CT_TB16NS16
+#define WT_CT_TB16NS16 8192
+#endif
+  static constexpr int BYTES = RB == 2 ? (WGStage<InT>::on ? WT_CT_TB16 : sizeof(InT) == 2 ? WT_CT_TB16NS16 : WT_CT_TB16NS)
+                                       : RB == 4 ? (WGStage<InT>::on ? WT_CT_TB : WT_CT_TB32NS)
+                                                 : (WGStage<InT>::on ? WT_CT_TB : WT_CT_TBNS);
   static constexpr int T = BYTES / RB;
   static constexpr int SPW = T / WGTile<RecT>::SC / CT_WARPS;  // superchunks per warp
   static_assert(SPW >= 1 && T % (WGTile<RecT>::SC * CT_WARPS) == 0, "whole superchunks per warp");

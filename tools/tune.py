@@ -9,9 +9,10 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "tune_variants")
 VARIANTS = {
     "base": [],
-    "t32ns_4k": ["WT_CT_TB32NS=16384"],
-    "t32ns_2k": ["WT_CT_TB32NS=8192", "WT_CT_TB16NS=10240"],
-    "t16ns_8k": ["WT_CT_TB16NS=16384"],
+    "ns16": ["WT_WG_STAGE16=0"],
+    "ns8": ["WT_WG_STAGE8=0"],
+    "ns8_12k": ["WT_WG_STAGE8=0", "WT_CT_TBNS=12288"],
+    "ns16_4k": ["WT_WG_STAGE16=0", "WT_CT_TB16NS=8192"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
