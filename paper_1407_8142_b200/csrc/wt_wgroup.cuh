@@ -370,13 +370,17 @@ __device__ __forceinline__ void run_blocks(uint32_t *bc, const uint32_t *LBw, co
     if (c) atomicAdd(bc + b, c);
   }
 }
+// `ones` returns the ones of the run's own bits when every word of it was
+// handled here (ni == 0), else ~0u (the caller falls back to rank queries)
 __device__ __forceinline__ uint32_t wg_run(unsigned long long &cw, uint8_t &cf, const uint32_t *LBw, uint64_t *B,
-                                           uint32_t n32, uint32_t G, uint32_t ls, uint32_t cnt) {
+                                           uint32_t n32, uint32_t G, uint32_t ls, uint32_t cnt, uint32_t &ones) {
   const uint32_t g0 = G & 63u, e = G + cnt;
   const uint32_t gw0 = G >> 6, gwl = (e - 1u) >> 6;
   WT_CHECK(cnt > 0 && (uint64_t)G + cnt <= n32, 203);
   const uint32_t hb = min(cnt, 64u - g0);
-  uint64_t head = lb_bits(LBw, ls, hb) << g0;
+  const uint64_t hbits = lb_bits(LBw, ls, hb);
+  uint32_t c = __popcll(hbits);
+  uint64_t head = hbits << g0;
   const uint32_t f = cf;
   bool shared = g0 != 0;
   if (f & CF_VALID) {
@@ -387,14 +391,19 @@ __device__ __forceinline__ uint32_t wg_run(unsigned long long &cw, uint8_t &cf, 
   if (gw0 == gwl && open_end) {
     cw = head;
     cf = CF_VALID | (shared ? CF_SHARED : 0);
+    ones = c;
     return 0u;
   }
   if (shared) atomicOr(reinterpret_cast<unsigned long long *>(&B[gw0]), (unsigned long long)head);
   else B[gw0] = head;
   cf = 0;
-  if (gw0 == gwl) return 0u;
+  if (gw0 == gwl) {
+    ones = c;
+    return 0u;
+  }
   const uint32_t tb = e - (gwl << 6);  // 1..64 bits in the last word
   const uint64_t tail = lb_bits(LBw, ls + cnt - tb, tb);
+  c += __popcll(tail);
   if (open_end) {
     cw = tail;
     cf = CF_VALID;
@@ -403,9 +412,15 @@ __device__ __forceinline__ uint32_t wg_run(unsigned long long &cw, uint8_t &cf, 
   }
   const uint32_t ni = gwl - gw0 - 1u;
   if (ni <= WT_WG_INLANE) {
-    for (uint32_t w = 0; w < ni; w++) B[gw0 + 1u + w] = lb_bits(LBw, ls + hb + 64u * w, 64);
+    for (uint32_t w = 0; w < ni; w++) {
+      const uint64_t x = lb_bits(LBw, ls + hb + 64u * w, 64);
+      c += __popcll(x);
+      B[gw0 + 1u + w] = x;
+    }
+    ones = c;
     return 0u;
   }
+  ones = ~0u;
   return ni;
 }
 
@@ -773,13 +788,17 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
             kk = 31 - __clz(slot);
             const uint32_t G = s.pos[slot], ls = s.S[slot];
             uint64_t *B = p.bits + (uint64_t)(p.l0 + kk) * p.wpl;
-            ni = wg_run(s.CW[slot], s.CF[slot], reinterpret_cast<const uint32_t *>(s.LB[kk]), B, n32, G, ls, cn);
+            uint32_t ones;
+            ni = wg_run(s.CW[slot], s.CF[slot], reinterpret_cast<const uint32_t *>(s.LB[kk]), B, n32, G, ls, cn, ones);
             gwA = (G >> 6) + 1;
             lsA = ls + min(cn, 64u - (G & 63u));
             s.pos[slot] = G + cn;
             Gr = G; lsr = ls; cnr = cn;
-            // fused A7: short runs count their blocks here, long ones below (lane per block)
-            if ((((G + cn - 1u) >> 9) - (G >> 9)) < 4u)
+            // fused A7: a run inside one 512-bit block adds the ones wg_run counted; other
+            // short runs count their blocks here, long ones below (lane per block)
+            if ((G >> 9) == ((G + cn - 1u) >> 9) && ones != ~0u) {
+              if (ones) atomicAdd(p.blkcnt + (uint64_t)(p.l0 + kk) * p.bpl + (G >> 9), ones);
+            } else if ((((G + cn - 1u) >> 9) - (G >> 9)) < 4u)
               run_blocks(p.blkcnt + (uint64_t)(p.l0 + kk) * p.bpl, reinterpret_cast<const uint32_t *>(s.LB[kk]),
                          s.RP[kk], G, ls, cn, G >> 9, (G + cn - 1u) >> 9, 1u);
           }
