@@ -13,9 +13,6 @@ constexpr int TW = WT_TW;                // elements per warp tile
 constexpr int NCH = TW / 32;             // 32-element chunks per tile
 constexpr int TAU_MAX = 8;               // levels fused per HBM pass
 constexpr int NDIG = 1 << TAU_MAX;       // digit values per pass
-constexpr uint32_t FLAG_AGG = 1u << 30;  // lookback: tile aggregate published
-constexpr uint32_t FLAG_INC = 2u << 30;  // lookback: inclusive prefix published
-constexpr uint32_t VAL_MASK = (1u << 30) - 1;
 
 #ifdef WT_DEBUG
 static __device__ uint32_t g_wt_dbg[4];

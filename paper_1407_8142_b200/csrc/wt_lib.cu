@@ -363,7 +363,11 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     chk(cudaEventRecord(ev0, s));
     chk(cudaStreamWaitEvent(side, ev0, 0));
     cudaEventDestroy(ev0);
-    chk(cudaMemsetAsync(t->bits + (uint64_t)G[g].l0 * WPL, 0, (uint64_t)G[g].tau * WPL * sizeof(uint64_t), side));
+    if (!G[g].local && !use_old_group() && !WT_BITS_MEMSET)
+      // k_wgroup writes every word of its levels (put_shared_word): only the padding
+      k_zero_pad<<<G[g].tau, 32, 0, side>>>(t->bits, WPL, (n + 63) / 64, G[g].l0);
+    else
+      chk(cudaMemsetAsync(t->bits + (uint64_t)G[g].l0 * WPL, 0, (uint64_t)G[g].tau * WPL * sizeof(uint64_t), side));
     if (blkcnt)
       chk(cudaMemsetAsync(blkcnt + (uint64_t)G[g].l0 * BPL, 0, (uint64_t)G[g].tau * BPL * sizeof(uint32_t), side));
     chk(cudaEventCreateWithFlags(&ev_zero[g], cudaEventDisableTiming));

@@ -129,7 +129,11 @@ __global__ void __launch_bounds__(512) k_chain_hist(const T *__restrict__ keys, 
   const uint4 *V = reinterpret_cast<const uint4 *>(ab);
   const uint32_t len = end - beg;
   const uint32_t nv = (uint32_t)(((uint64_t)head + len + PER - 1) / PER);
-  for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+  // vectors [1, nfull) lie wholly inside the chain: no per-element bounds
+  // checks there, two 16-byte loads in flight per thread; the (at most two)
+  // partial vectors at the ends take the checked path
+  const uint32_t nfull = (uint32_t)(((uint64_t)head + len) / PER);
+  auto vec_checked = [&](uint32_t i) {
     const uint4 q = __ldcs(V + i);
     const T *e = reinterpret_cast<const T *>(&q);
 #pragma unroll
@@ -137,7 +141,21 @@ __global__ void __launch_bounds__(512) k_chain_hist(const T *__restrict__ keys, 
       const int64_t pos = (int64_t)i * PER + k - head;
       if (pos >= 0 && pos < (int64_t)len) add((uint32_t)e[k]);
     }
+  };
+  auto vec_all = [&](const uint4 &q) {
+    const T *e = reinterpret_cast<const T *>(&q);
+#pragma unroll
+    for (int k = 0; k < PER; k++) add((uint32_t)e[k]);
+  };
+  if (threadIdx.x == 0) vec_checked(0);
+  if (nfull < nv && threadIdx.x == (nfull % blockDim.x) && nfull > 0) vec_checked(nfull);
+  uint32_t i = 1 + threadIdx.x;
+  for (; i + blockDim.x < nfull; i += 2 * blockDim.x) {
+    const uint4 q0 = __ldcs(V + i), q1 = __ldcs(V + i + blockDim.x);
+    vec_all(q0);
+    vec_all(q1);
   }
+  if (i < nfull) vec_all(__ldcs(V + i));
   __syncthreads();
   for (uint32_t d = threadIdx.x; d < ndig; d += blockDim.x) {
     uint32_t sum = 0;

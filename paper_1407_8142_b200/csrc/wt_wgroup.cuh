@@ -52,8 +52,9 @@
 // running position pos[slot], slot = 2^k + r, initialised per chain from V
 // and the row's digit scan (Cseg of wt_prep.cuh); words inside a run are
 // stored, the partial last word of a run is carried to the next tile of the
-// chain, words shared with another chain or node are OR-ed atomically into
-// the zero-initialised bitmap.  Each run also adds its ones to the 512-bit
+// chain, words shared with another chain or node get the writer's bits by an
+// atomic OR and an atomic AND confined to them (put_shared_word), so the
+// bitmap needs no zero initialisation (only its padding words are zeroed).  Each run also adds its ones to the 512-bit
 // blocks it overlaps (red.add into blkcnt; fused A7), so the
 // rank directory needs no second read of the bitmaps (k_rank_counts).
 #pragma once
@@ -66,6 +67,17 @@ namespace wtb {
 #define WT_CT_WARPS 4
 #endif
 constexpr int CT_WARPS = WT_CT_WARPS;  // warps of a CTA; they share one tile, each splits a quarter
+// cross-lane prefix of the split by a packed shfl.up scan over two superchunks
+// (8-bit records: measured faster; 16-bit: slower, the ballots stay)
+#ifndef WT_WG_SCAN
+#define WT_WG_SCAN 1
+#endif
+#ifndef WT_WG_SCAN16
+#define WT_WG_SCAN16 0
+#endif
+#ifndef WT_WG_PIPE
+#define WT_WG_PIPE 0
+#endif
 #ifndef WT_WG_UNROLL
 #define WT_WG_UNROLL 2
 #endif
@@ -177,6 +189,14 @@ __device__ __forceinline__ uint32_t ballot_m(uint32_t v, uint32_t m) {
       : "r"(v), "r"(m));
   return r;
 }
+// one step of an inclusive warp scan: v + (the value of lane - d, if it exists)
+__device__ __forceinline__ uint32_t shfl_up_add(uint32_t v, uint32_t d) {
+  asm volatile(
+      "{.reg .pred p; .reg .b32 t; shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff; @p add.u32 %0, %0, t;}"
+      : "+r"(v)
+      : "r"(d));
+  return v;
+}
 __device__ __forceinline__ uint32_t rev_bits(uint32_t x, uint32_t nb) { return nb ? __brev(x) >> (32u - nb) : 0u; }
 
 // ---------------------------------------------------------------------------
@@ -196,86 +216,112 @@ __device__ __forceinline__ void wg_split(uint8_t *LB, uint16_t *RP, uint32_t src
   uint32_t SP = SP0;                                // ones before the superchunk (level k)
   uint32_t Bo = dst + (Z + SP0) * RB;               // ones region + ones so far
   uint32_t Bz = dst + (c0 * SC - SP0) * RB + lane * LANEB;  // zeros so far + this lane's first slot
-  if constexpr (RB == 1) {
-    // software pipelined: the next superchunk's load is issued before this one is processed
-    uint2 xn = lds64(sA + c0 * (SC * RB));
-#pragma unroll(WG_UNROLL)
-    for (uint32_t c = c0; c < c1; c++) {
-      const uint2 x = xn;
-      if (c + 1 < c1) xn = lds64(sA + (c + 1) * (SC * RB));
-      const uint32_t t_lo = (x.x >> k) & 0x01010101u, t_hi = (x.y >> k) & 0x01010101u;
-      const uint32_t pre_lo = t_lo * 0x01010100u;
-      const uint32_t inc_lo = pre_lo + t_lo;
-      const uint32_t pre_hi = t_hi * 0x01010100u + __byte_perm(inc_lo, 0, 0x3333);
-      const uint32_t inc = pre_hi + t_hi;  // byte 3: ones of the lane (0..8)
-      const uint32_t O = __popc(ballot_m(inc, 1u << 24) & lt) + 2 * __popc(ballot_m(inc, 2u << 24) & lt) +
-                         4 * __popc(ballot_m(inc, 4u << 24) & lt) + 8 * __popc(ballot_m(inc, 8u << 24) & lt);
-      const uint32_t Sc = __shfl_sync(FULL, O + (inc >> 24), 31);
+  if constexpr (RB <= 2) {
+    // 8 records per lane: their digit bytes d (8-bit records: the records; 16-bit:
+    // the low bytes gathered by two PRMT), the level bits t, the exclusive in-lane
+    // prefix pre (SWAR: one IMAD per 4 bytes) and the lane's ones count (0..8)
+    struct Sw {
+      uint32_t t_lo, t_hi, pre_lo, pre_hi, cnt;
+    };
+    auto swar = [&](uint32_t d_lo, uint32_t d_hi) {
+      Sw w;
+      w.t_lo = (d_lo >> k) & 0x01010101u;
+      w.t_hi = (d_hi >> k) & 0x01010101u;
+      w.pre_lo = w.t_lo * 0x01010100u;
+      const uint32_t inc_lo = w.pre_lo + w.t_lo;
+      w.pre_hi = w.t_hi * 0x01010100u + __byte_perm(inc_lo, 0, 0x3333);
+      w.cnt = (w.pre_hi + w.t_hi) >> 24;
+      return w;
+    };
+    // superchunk c with the lane's exclusive cross-lane prefix O and the superchunk's ones Sc:
+    // word ranks, the level's bitmap byte, and (MOVE) the stable split of the records
+    auto emit = [&](uint32_t c, const Sw &w, uint32_t O, uint32_t Sc, uint32_t r0, uint32_t r1, uint32_t r2,
+                    uint32_t r3) {
       if (!(lane & 3)) sts16(rpA + (c * 8u + (lane >> 2)) * 2u, SP + O);
       // bits 24..27 <- elements 0..3, bits 28..31 <- elements 4..7 (disjoint products, no carries)
-      sts8(lbA + c * 32u + lane, (t_lo * 0x01020408u + t_hi * 0x10204080u) >> 24);
+      sts8(lbA + c * 32u + lane, (w.t_lo * 0x01020408u + w.t_hi * 0x10204080u) >> 24);
       if constexpr (MOVE) {
-        const uint32_t D0 = Bz - O;
-        const uint32_t A = (Bo + O - D0) | 0x10000u;
-        WT_CHECK(D0 >= dst && Bo + O + 8u <= dst + nsc * SC * RB + 8u, 201);
-        const uint32_t M_lo = t_lo * 0xffu, M_hi = t_hi * 0xffu;
-        const uint32_t q_lo = (pre_lo & M_lo) | ((0x03020100u - pre_lo) & ~M_lo);
-        const uint32_t q_hi = (pre_hi & M_hi) | ((0x07060504u - pre_hi) & ~M_hi);
-#pragma unroll
-        for (int w = 0; w < 2; w++) {
-          const uint32_t q = w ? q_hi : q_lo, t = w ? t_hi : t_lo, r = w ? x.y : x.x;
-          const uint32_t tq0 = __byte_perm(t, q, 0x5140), tq1 = __byte_perm(t, q, 0x7362);
-          sts8(__dp2a_lo(A, tq0, D0), r);
-          sts8(__dp2a_hi(A, tq0, D0), __byte_perm(r, 0, 0x1));
-          sts8(__dp2a_lo(A, tq1, D0), __byte_perm(r, 0, 0x2));
-          sts8(__dp2a_hi(A, tq1, D0), __byte_perm(r, 0, 0x3));
+        const uint32_t D0 = Bz - RB * O;
+        const uint32_t A = (Bo + RB * O - D0) | (RB << 16);
+        WT_CHECK(D0 >= dst && Bo + RB * O <= dst + nsc * SC * RB, 201);
+        const uint32_t M_lo = w.t_lo * 0xffu, M_hi = w.t_hi * 0xffu;
+        const uint32_t q_lo = (w.pre_lo & M_lo) | ((0x03020100u - w.pre_lo) & ~M_lo);
+        const uint32_t q_hi = (w.pre_hi & M_hi) | ((0x07060504u - w.pre_hi) & ~M_hi);
+        const uint32_t tq0 = __byte_perm(w.t_lo, q_lo, 0x5140), tq1 = __byte_perm(w.t_lo, q_lo, 0x7362);
+        const uint32_t tq2 = __byte_perm(w.t_hi, q_hi, 0x5140), tq3 = __byte_perm(w.t_hi, q_hi, 0x7362);
+        if constexpr (RB == 1) {
+          sts8(__dp2a_lo(A, tq0, D0), r0);
+          sts8(__dp2a_hi(A, tq0, D0), __byte_perm(r0, 0, 0x1));
+          sts8(__dp2a_lo(A, tq1, D0), __byte_perm(r0, 0, 0x2));
+          sts8(__dp2a_hi(A, tq1, D0), __byte_perm(r0, 0, 0x3));
+          sts8(__dp2a_lo(A, tq2, D0), r1);
+          sts8(__dp2a_hi(A, tq2, D0), __byte_perm(r1, 0, 0x1));
+          sts8(__dp2a_lo(A, tq3, D0), __byte_perm(r1, 0, 0x2));
+          sts8(__dp2a_hi(A, tq3, D0), __byte_perm(r1, 0, 0x3));
+        } else {
+          sts16(__dp2a_lo(A, tq0, D0), r0);
+          sts16(__dp2a_hi(A, tq0, D0), r0 >> 16);
+          sts16(__dp2a_lo(A, tq1, D0), r1);
+          sts16(__dp2a_hi(A, tq1, D0), r1 >> 16);
+          sts16(__dp2a_lo(A, tq2, D0), r2);
+          sts16(__dp2a_hi(A, tq2, D0), r2 >> 16);
+          sts16(__dp2a_lo(A, tq3, D0), r3);
+          sts16(__dp2a_hi(A, tq3, D0), r3 >> 16);
         }
       }
       SP += Sc;
-      Bo += Sc;
-      Bz += SC - Sc;
+      Bo += RB * Sc;
+      Bz += RB * (SC - Sc);
+    };
+    auto load = [&](uint32_t c, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+      if constexpr (RB == 1) {
+        const uint2 x = lds64(sA + c * (SC * RB));
+        r0 = x.x; r1 = x.y; r2 = r3 = 0u;
+      } else {
+        const uint4 x = lds128(sA + c * (SC * RB));
+        r0 = x.x; r1 = x.y; r2 = x.z; r3 = x.w;
+      }
+    };
+    auto digits_lo = [&](uint32_t r0, uint32_t r1) { return RB == 1 ? r0 : __byte_perm(r0, r1, 0x6420); };
+    auto digits_hi = [&](uint32_t r1, uint32_t r2, uint32_t r3) { return RB == 1 ? r1 : __byte_perm(r2, r3, 0x6420); };
+    uint32_t c = c0;
+    if constexpr ((RB == 1 && WT_WG_SCAN) || (RB == 2 && WT_WG_SCAN16)) {
+    // two superchunks per cross-lane prefix: the lanes' counts packed in 16-bit
+    // fields, one 5-step shfl.up scan (two instructions a step) for both
+    for (; c + 1 < c1; c += 2) {
+      uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+      load(c, a0, a1, a2, a3);
+      load(c + 1, b0, b1, b2, b3);
+      const Sw wa = swar(digits_lo(a0, a1), digits_hi(a1, a2, a3));
+      const Sw wb = swar(digits_lo(b0, b1), digits_hi(b1, b2, b3));
+      const uint32_t own = wa.cnt | (wb.cnt << 16);
+      uint32_t incl = own;
+#pragma unroll
+      for (uint32_t d = 1; d < 32; d <<= 1) incl = shfl_up_add(incl, d);
+      const uint32_t ex = incl - own, tot = __shfl_sync(FULL, incl, 31);
+      emit(c, wa, ex & 0xffffu, tot & 0xffffu, a0, a1, a2, a3);
+      emit(c + 1, wb, ex >> 16, tot >> 16, b0, b1, b2, b3);
     }
-  } else if constexpr (RB == 2) {
-    // 16-bit records: the level bits are in the low (digit) bytes, so the 8
-    // digit bytes of the lane are gathered (2 PRMT) and the 8-bit SWAR above
-    // runs unchanged; addresses step 2 bytes per record (A.hi = 2)
-    uint4 xn = lds128(sA + c0 * (SC * RB));
+    }
+    // one superchunk at a time: the cross-lane prefix from ballots of the count's bits;
+    // software pipelined (the next superchunk's load is issued before this one is processed)
+    uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+    if (WT_WG_PIPE && c < c1) load(c, n0, n1, n2, n3);
 #pragma unroll(WG_UNROLL)
-    for (uint32_t c = c0; c < c1; c++) {
-      const uint4 x = xn;
-      if (c + 1 < c1) xn = lds128(sA + (c + 1) * (SC * RB));
-      const uint32_t d_lo = __byte_perm(x.x, x.y, 0x6420), d_hi = __byte_perm(x.z, x.w, 0x6420);
-      const uint32_t t_lo = (d_lo >> k) & 0x01010101u, t_hi = (d_hi >> k) & 0x01010101u;
-      const uint32_t pre_lo = t_lo * 0x01010100u;
-      const uint32_t inc_lo = pre_lo + t_lo;
-      const uint32_t pre_hi = t_hi * 0x01010100u + __byte_perm(inc_lo, 0, 0x3333);
-      const uint32_t inc = pre_hi + t_hi;  // byte 3: ones of the lane (0..8)
+    for (; c < c1; c++) {
+      uint32_t a0, a1, a2, a3;
+      if (WT_WG_PIPE) {
+        a0 = n0; a1 = n1; a2 = n2; a3 = n3;
+        if (c + 1 < c1) load(c + 1, n0, n1, n2, n3);
+      } else {
+        load(c, a0, a1, a2, a3);
+      }
+      const Sw w = swar(digits_lo(a0, a1), digits_hi(a1, a2, a3));
+      const uint32_t inc = w.cnt << 24;
       const uint32_t O = __popc(ballot_m(inc, 1u << 24) & lt) + 2 * __popc(ballot_m(inc, 2u << 24) & lt) +
                          4 * __popc(ballot_m(inc, 4u << 24) & lt) + 8 * __popc(ballot_m(inc, 8u << 24) & lt);
-      const uint32_t Sc = __shfl_sync(FULL, O + (inc >> 24), 31);
-      if (!(lane & 3)) sts16(rpA + (c * 8u + (lane >> 2)) * 2u, SP + O);
-      sts8(lbA + c * 32u + lane, (t_lo * 0x01020408u + t_hi * 0x10204080u) >> 24);
-      if constexpr (MOVE) {
-        const uint32_t D0 = Bz - 2u * O;
-        const uint32_t A = (Bo + 2u * O - D0) | 0x20000u;
-        WT_CHECK(D0 >= dst && Bo + 2u * O <= dst + nsc * SC * RB, 201);
-        const uint32_t M_lo = t_lo * 0xffu, M_hi = t_hi * 0xffu;
-        const uint32_t q_lo = (pre_lo & M_lo) | ((0x03020100u - pre_lo) & ~M_lo);
-        const uint32_t q_hi = (pre_hi & M_hi) | ((0x07060504u - pre_hi) & ~M_hi);
-        const uint32_t tq0 = __byte_perm(t_lo, q_lo, 0x5140), tq1 = __byte_perm(t_lo, q_lo, 0x7362);
-        const uint32_t tq2 = __byte_perm(t_hi, q_hi, 0x5140), tq3 = __byte_perm(t_hi, q_hi, 0x7362);
-        sts16(__dp2a_lo(A, tq0, D0), x.x);
-        sts16(__dp2a_hi(A, tq0, D0), x.x >> 16);
-        sts16(__dp2a_lo(A, tq1, D0), x.y);
-        sts16(__dp2a_hi(A, tq1, D0), x.y >> 16);
-        sts16(__dp2a_lo(A, tq2, D0), x.z);
-        sts16(__dp2a_hi(A, tq2, D0), x.z >> 16);
-        sts16(__dp2a_lo(A, tq3, D0), x.w);
-        sts16(__dp2a_hi(A, tq3, D0), x.w >> 16);
-      }
-      SP += Sc;
-      Bo += 2u * Sc;
-      Bz += 2u * (SC - Sc);
+      const uint32_t Sc = __shfl_sync(FULL, O + w.cnt, 31);
+      emit(c, w, O, Sc, a0, a1, a2, a3);
     }
   } else {
 #pragma unroll 2
@@ -370,6 +416,30 @@ __device__ __forceinline__ void run_blocks(uint32_t *bc, const uint32_t *LBw, co
     if (c) atomicAdd(bc + b, c);
   }
 }
+// A5 without a zero-initialised bitmap (PAPER.md:430-439 CASes the <= 2
+// shared words of a node; here two order-independent atomics): a word shared
+// with other chains or nodes gets this writer's bits m set to v -- OR sets its
+// ones, AND clears its zeros, neither touches bits outside m -- so whatever
+// the word held before and in whatever order its writers come, every bit ends
+// as its owner wrote it.  Words a run owns entirely are stored; only the
+// level's padding words (beyond the last word holding a position < n) are
+// zeroed separately (k_zero_pad).  With WT_BITS_MEMSET the bitmap is zeroed
+// first and one atomicOr suffices.
+#ifndef WT_BITS_MEMSET
+#define WT_BITS_MEMSET 0
+#endif
+__device__ __forceinline__ void put_shared_word(uint64_t *w, uint64_t v, uint64_t m) {
+  atomicOr(reinterpret_cast<unsigned long long *>(w), (unsigned long long)v);
+  if (!WT_BITS_MEMSET) atomicAnd(reinterpret_cast<unsigned long long *>(w), (unsigned long long)(v | ~m));
+}
+constexpr uint32_t CF_LO_SHIFT = 2;  // carry flags: bits 2..7 = the chain's first bit in the carried word
+
+// zero the padding words [n64, wpl) of levels l0 .. l0+nl-1 (one block per level)
+static __global__ void k_zero_pad(uint64_t *bits, uint64_t wpl, uint64_t n64, uint32_t l0) {
+  uint64_t *B = bits + (uint64_t)(l0 + blockIdx.x) * wpl;
+  for (uint64_t w = n64 + threadIdx.x; w < wpl; w += blockDim.x) B[w] = 0;
+}
+
 // `ones` returns the ones of the run's own bits when every word of it was
 // handled here (ni == 0), else ~0u (the caller falls back to rank queries)
 __device__ __forceinline__ uint32_t wg_run(unsigned long long &cw, uint8_t &cf, const uint32_t *LBw, uint64_t *B,
@@ -383,18 +453,22 @@ __device__ __forceinline__ uint32_t wg_run(unsigned long long &cw, uint8_t &cf, 
   uint64_t head = hbits << g0;
   const uint32_t f = cf;
   bool shared = g0 != 0;
+  uint32_t lo = g0;  // the word's bits from lo up belong to this chain and slot
   if (f & CF_VALID) {
     head |= cw;
     shared = (f & CF_SHARED) != 0;
+    lo = f >> CF_LO_SHIFT;
   }
   const bool open_end = (e & 63u) != 0 && e != n32;  // the run's last word is unfinished
   if (gw0 == gwl && open_end) {
     cw = head;
-    cf = CF_VALID | (shared ? CF_SHARED : 0);
+    cf = CF_VALID | (shared ? CF_SHARED : 0) | (lo << CF_LO_SHIFT);
     ones = c;
     return 0u;
   }
-  if (shared) atomicOr(reinterpret_cast<unsigned long long *>(&B[gw0]), (unsigned long long)head);
+  // a written first word is ours from bit lo to 64 (a run ending inside it ends at n:
+  // the bits above n are zero padding, also ours)
+  if (shared) put_shared_word(&B[gw0], head, ~0ull << lo);
   else B[gw0] = head;
   cf = 0;
   if (gw0 == gwl) {
@@ -709,9 +783,10 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
       // ---- 2. tau levels of splits (bitmaps and word ranks kept per level) ----
       for (uint32_t k = 0; k < tau; k++) {
         uint32_t before = 0, tot = 0;
+        const uint32_t *cnts = s.onesW;
 #pragma unroll
         for (int w = 0; w < CT_WARPS; w++) {
-          const uint32_t o = s.onesW[w];
+          const uint32_t o = cnts[w];
           before += w < warp ? o : 0u;
           tot += o;
         }
@@ -855,7 +930,9 @@ __global__ void __launch_bounds__(CT_WARPS * 32) k_wgroup(GroupParams p) {
       if (s.CF[slot] & CF_VALID) {
         const uint32_t l = p.l0 + (31 - __clz(slot)), gw = s.pos[slot] >> 6;
         uint64_t *B = p.bits + (uint64_t)l * p.wpl;
-        atomicOr(reinterpret_cast<unsigned long long *>(&B[gw]), s.CW[slot]);
+        // the carried word holds this chain's bits [lo, pos & 63) (pos & 63 != 0: open end)
+        const uint32_t lo = s.CF[slot] >> CF_LO_SHIFT, hi = s.pos[slot] & 63u;
+        put_shared_word(&B[gw], s.CW[slot], (~0ull << lo) & ((1ull << hi) - 1ull));
       }
     }
     __syncthreads();

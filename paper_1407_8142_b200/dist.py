@@ -182,25 +182,29 @@ class ShardedPart:
         self.top = self.deep = None
 
 
-def build_sharded(S_local: torch.Tensor, sigma: int, comm=None, ops=None, gather: bool = True):
+def build_sharded(S_local: torch.Tensor, sigma: int, comm=None, ops=None, gather: bool = True,
+                  exchange: bool = False):
     """Build the wavelet tree of S = concat over ranks of S_local (rank order).
 
     Collective: every rank of ``comm`` must call it.  With ``gather`` (the
     default) every rank returns the complete tree (a ``WaveletTree`` with the
     CUDA ops); without, every rank returns its ``ShardedPart`` (distributed
-    output: no bitmap is all-gathered; ``assemble`` does it on demand)."""
-    part = _build_parts(S_local, sigma, comm, ops)
+    output: no bitmap is all-gathered; ``assemble`` does it on demand).
+    ``exchange`` runs the exchange steps even on a single rank (a one-rank
+    process group then carries the same all_to_all_single / all_gather calls
+    as P > 1; the tests use it to execute the NCCL path on one GPU)."""
+    part = _build_parts(S_local, sigma, comm, ops, exchange)
     if not isinstance(part, ShardedPart):
         return part
     return assemble(part, comm, ops) if gather else part
 
 
-def _build_parts(S_local: torch.Tensor, sigma: int, comm=None, ops=None):
+def _build_parts(S_local: torch.Tensor, sigma: int, comm=None, ops=None, exchange: bool = False):
     comm = comm if comm is not None else TorchComm()
     ops = ops if ops is not None else CudaOps()
     P, r = comm.world, comm.rank
     S_local = S_local.contiguous().view(-1)
-    if P == 1:  # nothing to exchange: the single-GPU build
+    if P == 1 and not exchange:  # nothing to exchange: the single-GPU build
         return ops.build(S_local, sigma)
     dev = S_local.device
     eb = S_local.element_size()

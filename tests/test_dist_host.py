@@ -1,5 +1,5 @@
-"""Host logic of the sharded build on CPU: world sizes 2
-and 3 over gloo (torch.distributed, 127.0.0.1), the local steps done by
+"""Host logic of the sharded build on CPU: world sizes 1
+(every exchange collective forced), 2 and 3 over gloo (torch.distributed, 127.0.0.1), the local steps done by
 tests/dist_helpers.HostOps (oracle chunk builds + numpy), the result compared
 array by array with the oracle's tree of the whole sequence."""
 from __future__ import annotations
@@ -53,12 +53,16 @@ def _worker(rank, world, port, q, cases):
             cuts[-1] = n
             if world == 3:
                 cuts = np.array([0, n // 5, n // 2, n])
+            if world == 1:
+                cuts = np.array([0, n])
             lo, hi = int(cuts[rank]), int(cuts[rank + 1])
-            t = wdist.build_sharded(torch.from_numpy(S[lo:hi].copy()), sigma, wdist.TorchComm(), HostOps())
+            # exchange=True: world size 1 still runs every exchange collective
+            t = wdist.build_sharded(torch.from_numpy(S[lo:hi].copy()), sigma, wdist.TorchComm(), HostOps(),
+                                    exchange=True)
             out.append(host_arrays(t))
             # distributed output: the same parts assembled on demand give the same tree
             part = wdist.build_sharded(torch.from_numpy(S[lo:hi].copy()), sigma, wdist.TorchComm(), HostOps(),
-                                       gather=False)
+                                       gather=False, exchange=True)
             if isinstance(part, wdist.ShardedPart):
                 # this rank's top-level runs: lengths are its class counts, offsets inside the level
                 for k in range(part.tau):
@@ -69,9 +73,9 @@ def _worker(rank, world, port, q, cases):
             else:
                 out[-1] = (out[-1], host_arrays(part))
         # invalid symbol on one rank only: every rank must raise
-        bad = np.array([1, 2, 3] if rank == 0 else [1, 9, 2], dtype=np.uint8)
+        bad = np.array([1, 2, 3] if rank == 0 and world > 1 else [1, 9, 2], dtype=np.uint8)
         try:
-            wdist.build_sharded(torch.from_numpy(bad), 4, wdist.TorchComm(), HostOps())
+            wdist.build_sharded(torch.from_numpy(bad), 4, wdist.TorchComm(), HostOps(), exchange=True)
             out.append("no error")
         except Exception as e:  # WtError(WT_ESYMBOL)
             out.append(getattr(e, "code", repr(e)))
@@ -82,7 +86,7 @@ def _worker(rank, world, port, q, cases):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [1, 2, 3])
 def test_sharded_build_gloo(world):
     import oracle
     ctx = mp.get_context("spawn")

@@ -124,7 +124,8 @@ def test_sharded_threads_config3():
         _cmp(got, want)
 
 
-def test_sharded_nccl_one_rank():
+@pytest.mark.parametrize("exchange", [False, True])
+def test_sharded_nccl_one_rank(exchange):
     import torch.distributed as dist
     from paper_1407_8142_b200 import dist as wdist
     from tests.dist_helpers import host_arrays
@@ -136,7 +137,9 @@ def test_sharded_nccl_one_rank():
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
         S = gen.uniform_below(300000, 1 << 16, seed=3, dtype=np.uint32)
-        t = wdist.build_sharded(torch.from_numpy(S).cuda(), 1 << 16)
+        # exchange=True: digit counts, top levels, all_to_all_single and the
+        # all-gathers of assemble() all go through NCCL (world size 1)
+        t = wdist.build_sharded(torch.from_numpy(S).cuda(), 1 << 16, exchange=exchange)
         _cmp(host_arrays(t), oracle.build(S, 1 << 16))
         t.free()
     finally:

@@ -249,3 +249,24 @@ def test_unaligned_narrow_types(dtype, sigma, off):
     tree = wt.build(v, sigma)
     _compare(S[off:].copy(), sigma, tree)
     tree.free()
+
+
+@pytest.mark.parametrize("n,sigma", [(300000, 1 << 16), (1 << 20, 256), (777777, 1 << 12), (5000, 1000)])
+def test_no_zero_init_dirty_memory(n, sigma):
+    """A5 without a zero-initialised bitmap (put_shared_word): the bitmap words
+    are written, never OR-ed into zeros, so a build whose output memory held
+    all-ones garbage (the freed bitmap of an earlier build, re-used by the
+    stream-ordered pool) is still bit-exact.  Each earlier tree's arrays are
+    filled with 0xff before it is freed."""
+    wt = _wt()
+    S = gen.uniform_below(n, sigma, seed=n % 97, dtype=_dtype_for(sigma))
+    St = torch.from_numpy(S).cuda()
+    for _ in range(3):
+        t = wt.build(St, sigma)
+        for k in ("bits", "rank_block", "rank_super", "node_key", "node_start"):
+            v = getattr(t, k)
+            if v is not None and v.numel():
+                v.view(torch.uint8).fill_(0xff)
+        torch.cuda.synchronize()
+        t.free()
+    _compare(S, sigma)

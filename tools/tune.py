@@ -6,17 +6,15 @@
 import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VDIR = os.path.join(ROOT, "tune_variants")
+VDIR = os.environ.get("TUNE_DIR", os.path.join(ROOT, "tune_variants"))
 VARIANTS = {
     "base": [],
-    "ns16": ["WT_WG_STAGE16=0"],
-    "ns8": ["WT_WG_STAGE8=0"],
-    "ns8_12k": ["WT_WG_STAGE8=0", "WT_CT_TBNS=12288"],
-    "ns16_4k": ["WT_WG_STAGE16=0", "WT_CT_TB16NS=8192"],
+    "nopipe": ["WT_WG_PIPE=0"],
+    "pipe_u1": ["WT_WG_UNROLL=1"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
-CPW = os.environ.get("TUNE_CPW", "4").split(",")
+CPW = os.environ.get("TUNE_CPW", "16").split(",")
 if sys.argv[1] == "build":
     from paper_1407_8142_b200 import _build
     os.makedirs(VDIR, exist_ok=True)
