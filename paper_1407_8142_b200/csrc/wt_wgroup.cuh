@@ -76,7 +76,7 @@ constexpr int CT_WARPS = WT_CT_WARPS;  // warps of a CTA; they share one tile, e
 #define WT_WG_SCAN16 0
 #endif
 #ifndef WT_WG_PIPE
-#define WT_WG_PIPE 0
+#define WT_WG_PIPE 1
 #endif
 #ifndef WT_WG_UNROLL
 #define WT_WG_UNROLL 2

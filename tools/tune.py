@@ -9,8 +9,9 @@ sys.path.insert(0, ROOT)
 VDIR = os.environ.get("TUNE_DIR", os.path.join(ROOT, "tune_variants"))
 VARIANTS = {
     "base": [],
-    "nopipe": ["WT_WG_PIPE=0"],
-    "pipe_u1": ["WT_WG_UNROLL=1"],
+    "t16_5k": ["WT_CT_TB16NS=10240"],
+    "t16_4k": ["WT_CT_TB16NS=8192"],
+    "t16_7k": ["WT_CT_TB16NS=14336"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
