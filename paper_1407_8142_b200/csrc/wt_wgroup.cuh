@@ -25,7 +25,7 @@
 // M_tau order, and rec >> tau is the key narrowed for the next group.
 //
 // The split (per level, per 32*E-position "superchunk", E = 8 (u8, u16
-// records) or 2 (u32)): lane l holds E consecutive records (one LDS.64 /
+// records) or 4 (u32)): lane l holds E consecutive records (one LDS.64 /
 // LDS.128); the level bits t_j, their exclusive in-lane prefix (SWAR: one IMAD
 // per 4 bytes), the lane's count and the cross-lane exclusive prefix O
 // (ballots of the count's bits + POPC) give every element its rank in its own
@@ -83,9 +83,14 @@ constexpr int CT_WARPS = WT_CT_WARPS;  // warps of a CTA; they share one tile, e
 #endif
 constexpr int WG_UNROLL = WT_WG_UNROLL;  // superchunks of the split loop unrolled
 
+// 32-bit records per lane per superchunk: 4 (one LDS.128; a third ballot of the
+// lane count, but half the cross-lane prefixes per record) or 2 (one LDS.64)
+#ifndef WT_WG_E32
+#define WT_WG_E32 4
+#endif
 template <typename RecT>
 struct WGTile {
-  static constexpr int E = sizeof(RecT) == 4 ? 2 : 8;  // records per lane per superchunk (one LDS)
+  static constexpr int E = sizeof(RecT) == 4 ? WT_WG_E32 : 8;  // records per lane per superchunk (one LDS)
   static constexpr int SC = 32 * E;                      // positions per superchunk
 };
 
@@ -323,6 +328,33 @@ __device__ __forceinline__ void wg_split(uint8_t *LB, uint16_t *RP, uint32_t src
       const uint32_t Sc = __shfl_sync(FULL, O + w.cnt, 31);
       emit(c, w, O, Sc, a0, a1, a2, a3);
     }
+  } else if constexpr (E == 4) {
+    // 32-bit records, four per lane: lane count 0..4 (three ballots), the lane's
+    // nibble of level bits paired with its neighbour's into one bitmap byte
+#pragma unroll 2
+    for (uint32_t c = c0; c < c1; c++) {
+      const uint4 x = lds128(sA + c * (SC * RB));
+      const uint32_t t0 = (x.x >> k) & 1u, t1 = (x.y >> k) & 1u, t2 = (x.z >> k) & 1u, t3 = (x.w >> k) & 1u;
+      const uint32_t p2 = t0 + t1, p3 = p2 + t2, tot = p3 + t3;
+      const uint32_t O = __popc(ballot_m(tot, 1u) & lt) + 2 * __popc(ballot_m(tot, 2u) & lt) +
+                         4 * __popc(ballot_m(tot, 4u) & lt);
+      const uint32_t Sc = __shfl_sync(FULL, O + tot, 31);
+      uint32_t v = t0 | (t1 << 1) | (t2 << 2) | (t3 << 3);
+      v |= __shfl_down_sync(FULL, v, 1) << 4;
+      if (!(lane & 7)) sts16(rpA + (c * 4u + (lane >> 3)) * 2u, SP + O);
+      if (!(lane & 1)) sts8(lbA + c * 16u + (lane >> 1), v);
+      if constexpr (MOVE) {
+        const uint32_t D0 = Bz - 4u * O, D1 = Bo + 4u * O;  // the lane's first zero / one slot
+        WT_CHECK(D0 >= dst && D1 <= dst + nsc * SC * RB, 201);
+        sts<uint32_t>(t0 ? D1 : D0, x.x);
+        sts<uint32_t>(t1 ? D1 + 4u * t0 : D0 + 4u * (1u - t0), x.y);
+        sts<uint32_t>(t2 ? D1 + 4u * p2 : D0 + 4u * (2u - p2), x.z);
+        sts<uint32_t>(t3 ? D1 + 4u * p3 : D0 + 4u * (3u - p3), x.w);
+      }
+      SP += Sc;
+      Bo += 4u * Sc;
+      Bz += 4u * (SC - Sc);
+    }
   } else {
 #pragma unroll 2
     for (uint32_t c = c0; c < c1; c++) {
@@ -363,6 +395,9 @@ __device__ __forceinline__ uint32_t wg_count(uint32_t src, uint32_t c0, uint32_t
     } else if constexpr (RB == 2) {
       const uint4 x = lds128(sA + c * (SC * RB));
       acc += ((__byte_perm(x.x, x.y, 0x6420) >> k) & 0x01010101u) + ((__byte_perm(x.z, x.w, 0x6420) >> k) & 0x01010101u);
+    } else if constexpr (E == 4) {
+      const uint4 x = lds128(sA + c * (SC * RB));
+      acc += ((x.x >> k) & 1u) + ((x.y >> k) & 1u) + ((x.z >> k) & 1u) + ((x.w >> k) & 1u);
     } else {
       const uint2 x = lds64(sA + c * (SC * RB));
       acc += ((x.x >> k) & 1u) + ((x.y >> k) & 1u);

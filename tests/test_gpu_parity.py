@@ -270,3 +270,22 @@ def test_no_zero_init_dirty_memory(n, sigma):
         torch.cuda.synchronize()
         t.free()
     _compare(S, sigma)
+
+
+# ---- 8 does not divide L: the first group takes the remainder ----
+@pytest.mark.parametrize("dtype,sigma", [(np.uint16, 1 << 9), (np.uint16, 1 << 10), (np.uint32, 1 << 10),
+                                         (np.uint16, 1 << 13), (np.uint32, 5000), (np.uint32, 1 << 15),
+                                         (np.uint32, 1 << 17), (np.uint32, 1 << 18), (np.uint32, 1 << 21),
+                                         (np.uint32, (1 << 23) - 1), (np.uint32, (1 << 26) + 3),
+                                         (np.uint32, 1 << 31)])
+def test_remainder_first_split(dtype, sigma):
+    """Chain mode in every group but the deepest (n is large enough that the
+    level-l0 rows of the first full group span many tiles): the first group has
+    tau = L mod 8 levels and writes keys narrowed to a multiple of 8 bits."""
+    n = 3_000_001
+    S = gen.uniform_below(n, sigma, seed=sigma % 1009, dtype=dtype)
+    _compare(S, sigma)
+    if sigma in (1 << 10, 1 << 18):
+        S = np.sort(S)
+        S[::7] = S[0]  # skew: one heavy symbol interleaved with ascending runs
+        _compare(S, sigma)

@@ -35,7 +35,7 @@ for k in [1, 2, 4, 6, 8, 10, 12, 14, 16, 18, 20, 24, 28, 32]:
                  "wt_sym_levels_per_s": N * k / (t1 * 1e-3), "wm_sym_levels_per_s": N * k / (t2 * 1e-3)})
     print(json.dumps(rows[-1]), flush=True)
     del S
-for e in [20, 22, 24, 26, 27, 28, 29, 30]:
+for e in ([] if os.environ.get("SWEEP_ONLY") == "sigma" else [20, 22, 24, 26, 27, 28, 29, 30]):
     n = 1 << e
     S = torch.from_numpy(gen.uniform_bits(n, 8, seed=200 + e, dtype=np.uint8)).cuda()
     t1 = timed(lambda: wt.build(S, 256))

@@ -9,9 +9,7 @@ sys.path.insert(0, ROOT)
 VDIR = os.environ.get("TUNE_DIR", os.path.join(ROOT, "tune_variants"))
 VARIANTS = {
     "base": [],
-    "t16_5k": ["WT_CT_TB16NS=10240"],
-    "t16_4k": ["WT_CT_TB16NS=8192"],
-    "t16_7k": ["WT_CT_TB16NS=14336"],
+    "e32_2": ["WT_WG_E32=2"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
