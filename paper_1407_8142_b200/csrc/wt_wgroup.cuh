@@ -40,13 +40,17 @@
 // per-tile digit histogram is built.  Padding records (all ones) fill the
 // last superchunk: they are ones at every level and stay at the end.
 //
-// Staging (north_star (2)): for 8-bit inputs (the 8-bit digit passes) tile
-// i+1's raw input (and, at a chain's last tile, the next chain's starting digit
-// counts V) is fetched by one cp.async.bulk per tile into `stage`, completing on
-// an mbarrier, while tile i is split.  16/32-bit inputs skip the stage (its
-// 2-4 B per position of shared memory buy larger tiles instead, measured
-// faster): the load step reads them with 16-byte loads, and the TMA unit
-// prefetches the next tile into L2 (cp.async.bulk.prefetch.L2) meanwhile.
+// Staging (north_star (2)): the TMA unit moves the next tile while the current
+// one is split.  Two forms, chosen per input width at compile time
+// (WT_WG_STAGE8/16/32): (a) staged -- tile i+1's raw input is fetched by one
+// cp.async.bulk into `stage`, completing on an mbarrier; (b) unstaged (the
+// default for every width since the end of round 2) -- the next tile is bulk-
+// prefetched into L2 (cp.async.bulk.prefetch.L2) and the load step reads it
+// with 16-byte loads; the stage's 1-4 B per position of shared memory buy a
+// sixth CTA per SM (8-bit inputs: k_group1 1.255 -> 1.197 ms on cfg4,
+// profiles/r02s5/tune_tiles8b.log) or larger tiles (16/32-bit inputs).  The
+// next chain's starting digit counts V always arrive by cp.async.bulk on the
+// mbarrier.
 //
 // Global placement (A5): class r of level k goes to the
 // running position pos[slot], slot = 2^k + r, initialised per chain from V
@@ -103,7 +107,7 @@ struct WGTile {
 #define WT_WG_STAGE16 0
 #endif
 #ifndef WT_WG_STAGE8
-#define WT_WG_STAGE8 1
+#define WT_WG_STAGE8 0
 #endif
 template <typename InT>
 struct WGStage {
@@ -125,8 +129,8 @@ struct WGStage {
 // records per tile: WT_CT_TB bytes of records (WT_CT_TB16 for 16-bit records of a staged
 // input); unstaged inputs use the stage's shared memory for larger tiles: 6144
 // 16-bit records of a 32-bit input, 4096 of a 16-bit input, 2048 32-bit records
-// (tools/tune.py).  8-bit inputs (the 8-bit digit passes) stay
-// TMA-staged: one cp.async.bulk per tile, one tile ahead.
+// (tools/tune.py).  8-bit inputs keep 8192-record tiles (larger
+// unstaged tiles lose the sixth CTA per SM: 10240 -> 1.254 ms, 12288 -> 1.309 ms).
 template <typename InT, typename RecT>
 struct WGSize {
   static constexpr int RB = sizeof(RecT);

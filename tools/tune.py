@@ -9,7 +9,9 @@ sys.path.insert(0, ROOT)
 VDIR = os.environ.get("TUNE_DIR", os.path.join(ROOT, "tune_variants"))
 VARIANTS = {
     "base": [],
-    "e32_2": ["WT_WG_E32=2"],
+    "stage8_0": ["WT_WG_STAGE8=0"],
+    "ns10k": ["WT_WG_STAGE8=0", "WT_CT_TBNS=10240"],
+    "ns12k": ["WT_WG_STAGE8=0", "WT_CT_TBNS=12288"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
