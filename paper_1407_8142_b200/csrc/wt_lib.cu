@@ -313,6 +313,9 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       const uint64_t target = (n + cpw * warps - 1) / (cpw * warps);
       const uint64_t tt = gb.gl.tile;
       gb.CH = std::max<uint64_t>(tt, ((target + tt - 1) / tt) * tt);
+      // one-tile chains pay the chain setup and the carried-word flush per tile: two tiles
+      // per chain while that still leaves >= 4 chains per worker (n = 10^8, 888 workers)
+      if (gb.CH == tt && n >= 8 * tt * warps) gb.CH = 2 * tt;
       gb.max_chains = g == 0 ? std::max<uint64_t>((n + gb.CH - 1) / gb.CH, 1)
                              : (n + gb.CH - 1) / gb.CH + gb.max_rows;
     }

@@ -9,9 +9,10 @@ sys.path.insert(0, ROOT)
 VDIR = os.environ.get("TUNE_DIR", os.path.join(ROOT, "tune_variants"))
 VARIANTS = {
     "base": [],
-    "stage8_0": ["WT_WG_STAGE8=0"],
-    "ns10k": ["WT_WG_STAGE8=0", "WT_CT_TBNS=10240"],
-    "ns12k": ["WT_WG_STAGE8=0", "WT_CT_TBNS=12288"],
+    "ns7k": ["WT_CT_TBNS=7168"],
+    "ns6k": ["WT_CT_TBNS=6144"],
+    "ns5k": ["WT_CT_TBNS=5120"],
+    "rp64": ["WT_WG_RP64=1"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
