@@ -422,6 +422,28 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     rec.end();
   };
 
+  // Work nothing on this stream waits for until the end of the build (the node tables of
+  // a group's levels, the block entries of a finished group) goes to the side stream:
+  // fork_side() orders the side stream after this stream's work so far; join_side()
+  // makes this stream wait for the node tables enqueued there so far (before the next
+  // group reads them); the end of the build waits for the whole side stream.  WT_NO_SIDE_A4: everything on this stream.
+  static const bool side_a4 = getenv("WT_NO_SIDE_A4") == nullptr;
+  cudaEvent_t ev_a4 = nullptr;  // the side stream's node tables so far
+  auto fork_side = [&]() {
+    cudaEvent_t ev;
+    chk(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    chk(cudaEventRecord(ev, s));
+    chk(cudaStreamWaitEvent(side, ev, 0));
+    cudaEventDestroy(ev);
+    side_used = true;
+  };
+  auto join_side = [&]() {
+    if (!ev_a4) return;
+    chk(cudaStreamWaitEvent(s, ev_a4, 0));
+    cudaEventDestroy(ev_a4);
+    ev_a4 = nullptr;
+  };
+
   if (small) {
     // ---- sigma <= 4: level 0 by ballots, level 1 as two compacted bit streams ----
     rec.begin("k_small_count", n * eb);
@@ -483,6 +505,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     } else if (G[g].local) {
       // ======== local mode: batches of small level-l0 nodes, finished per warp ========
       GroupBufs &gb = G[g];
+      join_side();  // the node tables of level l0
       rec.begin("k_rows", gb.max_rows * 8);
       k_rows_from_nodes<<<(unsigned)std::min<uint64_t>((gb.max_rows + 255) / 256, 65535), 256, 0, s>>>(
           t->level_node_ptr, ncount, gb.l0, t->node_key, t->node_start, gb.row_start, gb.row_key, gb.counts, err);
@@ -545,6 +568,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       continue;
     } else {
       GroupBufs &gb = G[g];
+      join_side();  // the node tables of level l0
       rec.begin("k_chains", gb.max_chains * 12);
       k_chains_from_nodes<<<1, 1024, 0, s>>>(t->level_node_ptr, ncount, gb.l0, t->node_key, t->node_start, n,
                                              gb.CH, gb.chain_begin, gb.chain_end, gb.chain_row, gb.row_first,
@@ -594,24 +618,36 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
       chk(cudaGetLastError());
       rec.end();
     } else if (gb.nk) {
+      // (side stream: it needs Cseg and the rows, and only the next group's chain setup
+      // and the end of the build need it; it overlaps k_chain_vec and the group pass)
       const uint64_t rstride = gb.max_rows;
       const unsigned cgrid = (unsigned)std::min<uint64_t>((gb.max_rows * gb.nk * 32 + 255) / 256, 65535);
-      rec.begin("k_nodes_count", 0);
-      k_row_nodes_count<<<cgrid, 256, 0, s>>>(gb.Cseg, gb.counts, gb.tau, gb.k_lo, gb.nk, rstride, gb.rowcnt, err);
+      cudaStream_t a4 = s;
+      if (side_a4) {
+        fork_side();
+        a4 = side;
+      }
+      rec.begin("k_nodes_count", 0, a4);
+      k_row_nodes_count<<<cgrid, 256, 0, a4>>>(gb.Cseg, gb.counts, gb.tau, gb.k_lo, gb.nk, rstride, gb.rowcnt, err);
       chk(cudaGetLastError());
-      k_scan_rows_1<<<dim3(gb.nblk, gb.nk), 1024, 0, s>>>(gb.rowcnt, rstride, gb.counts, gb.bsum, gb.nblk, err);
-      k_scan_rows_2<<<gb.nk, 1024, 0, s>>>(gb.bsum, gb.nblk, gb.counts, gb.l0, gb.k_lo, gb.nk, L, ncount,
-                                           t->level_node_ptr, err);
-      k_scan_rows_3<<<dim3(gb.nblk, gb.nk), 1024, 0, s>>>(gb.rowcnt, rstride, gb.counts, gb.bsum, gb.nblk, err);
-      k_level_ptr<<<1, 32, 0, s>>>(ncount, gb.l0, gb.k_lo, gb.nk, L, t->level_node_ptr, err);
+      k_scan_rows_1<<<dim3(gb.nblk, gb.nk), 1024, 0, a4>>>(gb.rowcnt, rstride, gb.counts, gb.bsum, gb.nblk, err);
+      k_scan_rows_2<<<gb.nk, 1024, 0, a4>>>(gb.bsum, gb.nblk, gb.counts, gb.l0, gb.k_lo, gb.nk, L, ncount,
+                                            t->level_node_ptr, err);
+      k_scan_rows_3<<<dim3(gb.nblk, gb.nk), 1024, 0, a4>>>(gb.rowcnt, rstride, gb.counts, gb.bsum, gb.nblk, err);
+      k_level_ptr<<<1, 32, 0, a4>>>(ncount, gb.l0, gb.k_lo, gb.nk, L, t->level_node_ptr, err);
       chk(cudaGetLastError());
       rec.end();
-      rec.begin("k_nodes_emit", 0);
-      k_row_nodes_emit<<<cgrid, 256, 0, s>>>(gb.Cseg, gb.counts, gb.tau, gb.l0, gb.k_lo, gb.nk, rstride, gb.rowcnt,
-                                             t->level_node_ptr, gb.row_key, gb.row_start, t->node_key,
-                                             t->node_start, err);
+      rec.begin("k_nodes_emit", 0, a4);
+      k_row_nodes_emit<<<cgrid, 256, 0, a4>>>(gb.Cseg, gb.counts, gb.tau, gb.l0, gb.k_lo, gb.nk, rstride, gb.rowcnt,
+                                              t->level_node_ptr, gb.row_key, gb.row_start, t->node_key,
+                                              t->node_start, err);
       chk(cudaGetLastError());
       rec.end();
+      if (a4 == side) {
+        if (ev_a4) cudaEventDestroy(ev_a4);
+        chk(cudaEventCreateWithFlags(&ev_a4, cudaEventDisableTiming));
+        chk(cudaEventRecord(ev_a4, side));
+      }
     }
     // ---- the fused tau-level pass ----
     GroupParams gp{};
@@ -650,10 +686,15 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
     if (blkcnt) {
       // fused A7: the pass accumulated the block popcounts; scan them per superblock
       if (NSD) {
-        rec.begin("k_rank_counts", (uint64_t)gb.tau * (BPL * 4 + BPL * 2 + NSD * 8));
+        cudaStream_t rs = s;
+        if (side_a4 && has_out) {  // a later group follows: overlap its chain setup
+          fork_side();
+          rs = side;
+        }
+        rec.begin("k_rank_counts", (uint64_t)gb.tau * (BPL * 4 + BPL * 2 + NSD * 8), rs);
         const uint64_t warps = (uint64_t)gb.tau * NSD;
-        k_rank_counts<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(blkcnt, BPL, NSD, gb.l0, gb.tau,
-                                                                            t->rank_block, suptot, err);
+        k_rank_counts<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, rs>>>(blkcnt, BPL, NSD, gb.l0, gb.tau,
+                                                                             t->rank_block, suptot, err);
         chk(cudaGetLastError());
         rec.end();
       }
@@ -680,6 +721,7 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   }
 
   if (ev_side) cudaEventDestroy(ev_side);
+  if (ev_a4) cudaEventDestroy(ev_a4);
   for (uint32_t g = 0; g < 8; g++) {  // groups that never launched (errors): keep s ordered
     if (ev_zero[g]) {
       chk(cudaStreamWaitEvent(s, ev_zero[g], 0));

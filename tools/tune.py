@@ -9,10 +9,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.environ.get("TUNE_DIR", os.path.join(ROOT, "tune_variants"))
 VARIANTS = {
     "base": [],
-    "ns7k": ["WT_CT_TBNS=7168"],
-    "ns6k": ["WT_CT_TBNS=6144"],
-    "ns5k": ["WT_CT_TBNS=5120"],
-    "rp64": ["WT_WG_RP64=1"],
+    "stage8": ["WT_WG_STAGE8=1"],
+    "e32_2": ["WT_WG_E32=2"],
 }
 if os.environ.get("TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["TUNE_ONLY"].split(",")}
