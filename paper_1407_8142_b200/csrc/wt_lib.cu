@@ -427,7 +427,10 @@ int build_impl(const void *d_seq, const void *h_seq, bool from_host, uint64_t n,
   // fork_side() orders the side stream after this stream's work so far; join_side()
   // makes this stream wait for the node tables enqueued there so far (before the next
   // group reads them); the end of the build waits for the whole side stream.  WT_NO_SIDE_A4: everything on this stream.
-  static const bool side_a4 = getenv("WT_NO_SIDE_A4") == nullptr;
+  // Not while kernel events are recorded (wt_profile_enable): a side-stream interval would
+  // include the wait for SM slots behind the persistent group pass, not the kernel's time.
+  static const bool side_a4_env = getenv("WT_NO_SIDE_A4") == nullptr;
+  const bool side_a4 = side_a4_env && !rec.timed;
   cudaEvent_t ev_a4 = nullptr;  // the side stream's node tables so far
   auto fork_side = [&]() {
     cudaEvent_t ev;
